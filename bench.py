@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the pJDS spMVM hot path (BASELINE.json metric: pJDS DP spMVM GFlop/s and HBM GB/s
+(% roofline) at 1/2/4/8 B200; bytes vs ELLPACK-R).
+
+One step = one y = A x over the whole matrix (SURVEY §8(a) a7+a8 at N=1; a12 = local part
+overlapped with the NCCL halo exchange + nonlocal part at N>1).  Default workload C5: HMEp-shaped
+Holstein-Hubbard matrix, M = 25 phonons, N = 57,002,400, nnz = 942,439,680, DP, synthetic values
+(inputs/gen.cpp), the same matrix for every N (strong scaling, rows partitioned on e-block
+boundaries of the nested spin-grid ordering).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C5] [--dtype f64|f32] [--impl pjds|ellr|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream around exactly K
+steps, barrier + synchronize on both sides, max over ranks.  The matrix (12.2 GB at C5 DP) is far
+larger than L2, so no explicit flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_DESC = {
+    "C1": "tiny HMEp-shaped banded N=16384",
+    "C2": "sAMG-shaped 7-point Poisson 150x150x151 Morton, N=3397500",
+    "C3": "HMEp Holstein-Hubbard M=15, N=6201600",
+    "C4": "DLR1-shaped 46417 points x 6, N=278502",
+    "C5": "HMEp Holstein-Hubbard M=25 nested spin-grid, N=57002400",
+}
+METRIC = "pJDS DP spMVM GFlop/s & HBM GB/s (% roofline) at 1/2/4/8 B200; bytes vs ELLPACK-R"
+# electronic-block size P (rows per contiguous off-diagonal segment) for partitioning
+SEGMENT = {"C1": 1024, "C3": 15504, "C5": 142506}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="pjds", choices=["pjds", "ellr", "reference"])
+    p.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
+    p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--block-rows", type=int, default=32)
+    p.add_argument("--no-overlap", action="store_true", help="dist: vector mode (exchange, then compute)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--probe-bytes", type=int, default=4 << 30)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self._nv = None
+            self.error = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                self.reasons |= self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        if not self._nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        r = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": r, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------------ CPU baseline
+def cpu_baseline(cfg: str, npdt, budget_s: float = 12.0):
+    """The oracle's plain CRS loop (oracle_spmv_crs, OpenMP static over rows, all visible cores) on a
+    bounded sample of the workload: a leading row block of the matrix, repeated until ~budget_s."""
+    import inputs
+    import oracle
+    g = inputs.Generator.from_config(cfg)
+    rows = min(g.n, 4_000_000)
+    rp, col, val = g.crs(0, rows, dtype=npdt)
+    x = inputs.vector(g.n, npdt)
+    cores = len(os.sched_getaffinity(0))
+    nnz = int(rp[-1])
+    oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)  # warm-up
+    ts = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end and len(ts) < 50:
+        t0 = time.perf_counter()
+        oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    return {"value": 2.0 * nnz / t / 1e9, "unit": "GFlop/s", "cores": cores, "kind": "oracle",
+            "sample": f"rows [0,{rows}) of {cfg} ({nnz} nnz), {len(ts)} reps, median, "
+                      f"{sum(ts):.1f} s CPU time, oracle_spmv_crs {np.dtype(npdt).name}"}
+
+
+# ------------------------------------------------------------------------------------------ main
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    npdt = np.float64 if a.dtype == "f64" else np.float32
+    sv = np.dtype(npdt).itemsize
+
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        return reference_arm(a, world, npdt)
+
+    import torch
+    import inputs
+    import paper_1112_5588_b200 as pj
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tdt = torch.float64 if npdt == np.float64 else torch.float32
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    t_setup = time.perf_counter()
+    g = inputs.Generator.from_config(a.config)
+    n = g.n
+    if world > 1:
+        seg = SEGMENT.get(a.config, 32)
+        nb = n // seg
+        offs = np.array([(nb * r // world) * seg for r in range(world + 1)], np.int64)
+        offs[-1] = n
+    else:
+        offs = np.array([0, n], np.int64)
+    lo, hi = int(offs[rank]), int(offs[rank + 1])
+    rp, col, val = g.crs(lo, hi, dtype=npdt)
+    nnz_loc = int(rp[-1])
+    if world > 1:
+        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows)
+        A_loc, A_nl = D.parts()
+        stats = {"local_part": A_loc.info, "nonlocal_part": A_nl.info if A_nl else None, "dist": D.info}
+        A = None
+    else:
+        if a.impl == "ellr":
+            A = pj.EllrMatrix.from_crs(n, rp, col, val)
+        else:
+            A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows)
+        stats = A.info
+    # footprint comparison (host-side accounting of both formats, bytes vs ELLPACK-R)
+    footprint = None
+    if world == 1:
+        if a.impl == "pjds":
+            ell_entries = (n + 31) // 32 * 32 * stats["len_max"]
+            footprint = {"pjds_bytes": stats["bytes_total"], "pjds_stored": stats["stored"],
+                         "ellr_bytes": ell_entries * (sv + 4) + (n + 31) // 32 * 32 * 4, "ellr_stored": ell_entries,
+                         "data_reduction_vs_ellpack": stats["data_reduction_vs_ellpack"]}
+            footprint["bytes_ratio_pjds_over_ellr"] = footprint["pjds_bytes"] / footprint["ellr_bytes"]
+    del col, val
+    nnz = nnz_loc
+    if world > 1:
+        t = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        nnz = int(t.item())
+    x = torch.from_numpy(inputs.vector(hi - lo, npdt, i0=lo)).to(dev)
+    y = torch.empty(hi - lo, dtype=tdt, device=dev)
+    t_setup = time.perf_counter() - t_setup
+
+    # roofline denominator measured in this run (copy and read streams; max taken)
+    probe_copy, probe_read = pj.bw_probe(a.probe_bytes, 5)
+    peaks = measured_peaks()
+    peak_file = peaks.get("hbm_gbs")
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if world > 1:
+            D.spmv(y, x, stream=stream, no_overlap=a.no_overlap)
+        else:
+            A.spmv(y, x, stream=stream)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = pj.launch_count()
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = pj.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    t_s = ms * 1e-3
+    gflops = 2.0 * nnz / t_s / 1e9
+    # algorithmic bytes (Eq. 1 at alpha = 1/N_nzr, write-only y): val+col once, x once, y once
+    b_min = nnz * (sv + 4) + 2 * n * sv
+    achieved = b_min / t_s / 1e9 / world  # per GPU
+    peak = peak_file if peak_file else max(probe_copy, probe_read)
+
+    # end-to-end through the public API with host buffers (H2D x, kernel, D2H y per step)
+    e2e = None
+    if world == 1 and a.impl == "pjds":
+        xh = torch.from_numpy(inputs.vector(n, npdt)).pin_memory().numpy()
+        yh = torch.empty(n, dtype=tdt).pin_memory().numpy()
+        A.spmv_host(yh, xh)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            A.spmv_host(yh, xh)
+        te = (time.perf_counter() - t0) / a.e2e_steps
+        e2e = {"value": 2.0 * nnz / te / 1e9, "unit": "GFlop/s", "h2d_bytes_per_step": n * sv,
+               "d2h_bytes_per_step": n * sv, "ms_per_step": te * 1e3}
+    elif world > 1:
+        e2e = {"value": None, "unit": "GFlop/s", "note": "host-buffer e2e is measured at N=1 only",
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a.config, npdt)
+
+    if rank == 0:
+        wl = f"{a.config}: {CONFIG_DESC[a.config]}, nnz={nnz}, {a.dtype}, {a.impl}"
+        out = {
+            "metric": METRIC,
+            "value": round(gflops, 2), "unit": "GFlop/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
+            "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows,
+                       "parallelism": f"row-partition r{world}" if world > 1 else "single GPU",
+                       "overlap": (not a.no_overlap) if world > 1 else None,
+                       "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
+            "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peak_file else "bw probe (this run)",
+                         "probe_copy_gbs": round(probe_copy, 1), "probe_read_gbs": round(probe_read, 1),
+                         "frac_of_probe_max": round(achieved / max(probe_copy, probe_read), 4),
+                         "algorithmic_bytes_per_step": b_min},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "footprint": footprint,
+            "setup_s": round(t_setup, 2),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        D.close()
+        dist.destroy_process_group()
+    return 0
+
+
+def reference_arm(a, world, npdt):
+    """--impl reference: the oracle (plain CRS, OpenMP over all host cores) on the same config,
+    metric and unit; each step is a bounded sample of the workload (a leading row block)."""
+    import inputs
+    import oracle
+    g = inputs.Generator.from_config(a.config)
+    rows = min(g.n, 4_000_000)
+    rp, col, val = g.crs(0, rows, dtype=npdt)
+    x = inputs.vector(g.n, npdt)
+    cores = len(os.sched_getaffinity(0))
+    nnz = int(rp[-1])
+    for _ in range(max(a.warmup, 1)):
+        oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)
+    steps = a.steps
+    t0 = time.perf_counter()
+    deadline = t0 + 120.0
+    done = 0
+    while done < steps and time.perf_counter() < deadline:
+        oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)
+        done += 1
+    t = (time.perf_counter() - t0) / done
+    v = 2.0 * nnz / t / 1e9
+    sample = f"rows [0,{rows}) of {a.config} ({nnz} nnz) per step, {done} steps"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC,
+        "value": round(v, 3), "unit": "GFlop/s", "n_gpus": world, "steps": done, "warmup": max(a.warmup, 1),
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": a.dtype, "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
+        "config": {"workload": f"{a.config}: {CONFIG_DESC[a.config]}, CPU oracle CRS (sample)"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GFlop/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,234 @@
+/*
+ * pjds.h — C ABI of libpjds: sparse matrix-vector multiplication y = A x in the padded jagged
+ * diagonals storage (pJDS) format of Kreutzer, Hager, Wellein, Fehske, Basermann, Bishop,
+ * "Sparse matrix-vector multiplication on GPGPU clusters: A new storage format and a scalable
+ * implementation" (arXiv 1112.5588; cited as PAPER.md L<line>), with ELLPACK-R as the in-library
+ * comparison format, on NVIDIA B200 (sm_100a).
+ *
+ * Conventions for every entry point
+ *   - Return value: pjds_status (0 = PJDS_OK, < 0 = error).  Nothing aborts; on error a
+ *     thread-local message is available from pjds_last_error().
+ *   - Host arrays passed to *_create* are only read during the call (the caller keeps ownership).
+ *   - Handles own all device memory they allocate until *_destroy.
+ *   - x / y in *_spmv are caller-owned DEVICE pointers on the handle's device with the handle's
+ *     dtype (float for PJDS_F32, double for PJDS_F64); y must not alias x (PJDS_ERR_INVALID_ARG).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is enqueued
+ *     and the call returns; launch errors are returned immediately, asynchronous faults surface
+ *     at the caller's next synchronisation.
+ *   - Preconditions on values: x must be finite (padding slots compute +0.0 * x[0], reading 7).
+ *   - Index types: rowptr int64, column indices int32 (n < 2^31), offsets int64.
+ */
+#ifndef PJDS_H
+#define PJDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pjds_mat* pjds_t;
+typedef struct ellr_mat* ellr_t;
+typedef struct pjds_plan* pjds_plan_t;
+typedef struct pjds_dist* pjds_dist_t;
+
+typedef enum { PJDS_F32 = 0, PJDS_F64 = 1 } pjds_dtype;
+
+typedef enum {
+  PJDS_OK = 0,
+  PJDS_ERR_INVALID_ARG = -1, /* null pointer, bad size, bad block_rows, aliasing, wrong mode */
+  PJDS_ERR_BAD_CSR = -2,     /* rowptr[0] != 0, decreasing rowptr, column out of range */
+  PJDS_ERR_OOM = -3,         /* host or device allocation failed */
+  PJDS_ERR_CUDA = -4,        /* CUDA runtime error (message has cudaGetErrorString) */
+  PJDS_ERR_NCCL = -5,        /* NCCL missing or failed (message has ncclGetErrorString) */
+  PJDS_ERR_UNSUPPORTED = -6  /* feature not available in this build / on this device */
+} pjds_status;
+
+/* create flags */
+enum {
+  PJDS_PERM_ROWS = 0u,      /* default: rows permuted only; x and y in the ORIGINAL basis,
+                               y stored through perm (reading 9) */
+  PJDS_PERM_SYMMETRIC = 1u, /* permuted basis: columns mapped through
+                               invperm, x and y both in the permuted basis (P A P^T) */
+  PJDS_HOST_ONLY = 2u       /* convert on the host only, no device allocation (export/info
+                               work, spmv returns PJDS_ERR_INVALID_ARG); used by CPU tests */
+};
+
+/* ------------------------------------------------------------------ single-GPU formats */
+
+/*
+ * pjds_create_from_crs — CRS -> pJDS, §2.1 L213-229 and Listing 2:
+ *   a1 row lengths (stored CRS entries, explicit zeros and duplicates count);
+ *   a2 "sort": rows by descending length, ties by ascending original row (stable), perm[new]=old;
+ *   a3 "pad": n_pad = ceil(n/block_rows)*block_rows with zero-length virtual rows, every block of
+ *      block_rows consecutive sorted rows padded to its longest row: block_len[b] (non-increasing);
+ *   a4 col_start[j] (j = 0..width, width = block_len[0]): offset of jagged column j,
+ *      col_start[j+1] = col_start[j] + block_rows * #{b : block_len[b] > j};
+ *   a5 fill: val[col_start[j] + k] = j-th stored entry of sorted row k (CRS order kept),
+ *      padding (+0.0, column 0); then one upload to the current CUDA device.
+ *  n          rows = columns (square), 0 <= n < 2^31
+ *  rowptr     host int64[n+1], rowptr[0] = 0, non-decreasing
+ *  col        host int32[rowptr[n]], 0 <= col < n
+ *  val        host float[] / double[] per dtype, rowptr[n] entries
+ *  block_rows b_r: a positive multiple of 32 (warp size); 0 means 32
+ *  flags      PJDS_PERM_* | PJDS_HOST_ONLY
+ */
+int pjds_create_from_crs(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col,
+                         const void* val, int dtype, int32_t block_rows, uint32_t flags);
+int pjds_destroy(pjds_t A);
+
+/*
+ * pjds_spmv — y = A x (overwrite; reading 11) with the pJDS kernel (Listing 2,
+ * PAPER.md L231-237; one thread per row, rows of a warp in one block).
+ * Per row: one fused multiply-add chain over the row's stored entries in CRS order, starting
+ * from +0.0, in the matrix precision; padded slots add exact +0.  Rows of length 0 give y = +0.
+ * PJDS_PERM_ROWS: x, y original basis.  PJDS_PERM_SYMMETRIC: x, y permuted basis.
+ */
+int pjds_spmv(pjds_t A, void* y, const void* x, void* stream);
+
+/*
+ * pjds_spmv_host — end-to-end variant with HOST x / y (any host memory; pinned is faster):
+ * copies x host->device, runs pjds_spmv, copies y device->host, and synchronises `stream`.
+ * The transfer cost is the paper's T_PCI (Eq. 2).  Staging buffers are
+ * allocated on first use and owned by the handle.
+ */
+int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream);
+
+typedef struct {
+  int64_t n, nnz, n_pad, n_blocks, stored;
+  int32_t block_rows, width, dtype, flags;
+  int32_t len_min, len_max;
+  double len_mean;
+  /* Fig. 2 counters, lane-slots: useful = nnz, padded = stored - nnz
+     (executed as +0 FMAs), idle = 0 (every lane of a block runs block_len steps) */
+  int64_t useful_fma, padded_fma, idle_lane_slots;
+  /* footprint (Table 1): values, int32 column indices,
+     aux = col_start (int64, width+1) + block_len (int32, n_blocks) + perm (int32, n) */
+  int64_t bytes_values, bytes_indices, bytes_aux, bytes_total;
+  double data_reduction_vs_ellpack; /* 1 - stored / (ceil(n/32)*32 * width), entries basis */
+  int32_t on_device;
+  int32_t device;
+} pjds_info_t;
+
+int pjds_info(pjds_t A, pjds_info_t* out);
+
+/* Row-length histogram (Fig. 3, bin size 1): counts[L] = #rows of length L
+   for L < nbins (rows longer than nbins-1 are not counted). */
+int pjds_histogram(pjds_t A, int64_t* counts, int32_t nbins);
+
+/* Copy the format arrays into caller HOST buffers sized from pjds_info: perm[n],
+   block_len[n_blocks], col_start[width+1], col[stored], val[stored] (any may be NULL). */
+int pjds_export(pjds_t A, int32_t* perm, int32_t* block_len, int64_t* col_start, int32_t* col,
+                void* val);
+
+/*
+ * ellr_create_from_crs — CRS -> ELLPACK-R: entries shifted
+ * left, N_pad = ceil(n/32)*32 rows x width = N^max_nzr columns stored column by column
+ * (val[j*N_pad + i]), padding (+0.0, col 0), rowmax[i] = row length (0 for pad rows).
+ * Same argument rules as pjds_create_from_crs (flags: 0 or PJDS_HOST_ONLY).
+ */
+int ellr_create_from_crs(ellr_t* out, int64_t n, const int64_t* rowptr, const int32_t* col,
+                         const void* val, int dtype, uint32_t flags);
+int ellr_destroy(ellr_t A);
+/* y = A x with the ELLPACK-R kernel (Listing 1), same chain semantics. */
+int ellr_spmv(ellr_t A, void* y, const void* x, void* stream);
+
+typedef struct {
+  int64_t n, nnz, n_pad, stored;
+  int32_t width, dtype;
+  int64_t useful_fma, padded_fma, idle_lane_slots; /* idle = sum_warps sum_lanes (max - len) */
+  int64_t bytes_values, bytes_indices, bytes_aux, bytes_total; /* aux = rowmax int32[n_pad] */
+  int32_t on_device, device;
+} ellr_info_t;
+int ellr_info(ellr_t A, ellr_info_t* out);
+int ellr_export(ellr_t A, int32_t* rowmax, int32_t* col, void* val);
+
+/* ------------------------------------------------------------------ distributed (§3) */
+
+/*
+ * Row-partitioned spMVM.  Rank r owns rows and x entries
+ * [row_offsets[r], row_offsets[r+1]).  Its rows are split into a local part (columns it owns)
+ * and a nonlocal part (columns owned by other ranks); the nonlocal x entries
+ * (halo) are exchanged with NCCL send/recv on a high-priority side stream while the local part
+ * runs (task mode), then the nonlocal part accumulates y += (the result is
+ * written twice, L445).
+ *
+ * Setup is three steps so that the only cross-rank setup traffic (index lists) is plumbing done
+ * by the caller (e.g. torch.distributed all_to_all):
+ *   1. pjds_dist_plan      (local, host): split + recv lists.  Halo schedule conventions:
+ *                          recv list from owner q = sorted unique global columns owned by q;
+ *                          halo slot = position in the concatenation ordered by owner rank.
+ *   2. caller exchanges recv lists -> send lists (what each peer needs from this rank).
+ *   3. pjds_dist_create    builds A_loc (all local rows, local column ids) and A_nl (rows with
+ *                          >= 1 nonlocal entry, halo-slot column ids), both pJDS, uploads, and
+ *                          sets up the transport.
+ */
+int pjds_dist_plan(pjds_plan_t* out, int32_t nranks, int32_t rank, int64_t n_global,
+                   const int64_t* row_offsets /* [nranks+1] */,
+                   const int64_t* rowptr_loc /* [n_loc+1], rowptr_loc[0] = 0 */,
+                   const int32_t* col_global_loc /* global column ids of this rank's rows */);
+typedef struct {
+  int64_t n_loc, nnz_loc, nnz_local_part, nnz_nonlocal_part, rows_nonlocal, halo;
+  int32_t nranks, rank;
+} pjds_plan_info_t;
+int pjds_dist_plan_info(pjds_plan_t P, pjds_plan_info_t* out);
+/* recv_counts[nranks]; recv_cols[halo] (global ids, owner-ordered); either may be NULL */
+int pjds_dist_plan_recv(pjds_plan_t P, int64_t* recv_counts, int32_t* recv_cols);
+int pjds_dist_plan_destroy(pjds_plan_t P);
+
+enum {
+  PJDS_TRANSPORT_NCCL = 0,  /* one process per GPU; nccl_unique_id = 128-byte ncclUniqueId */
+  PJDS_TRANSPORT_LOCAL = 1  /* all ranks' handles in this process (pjds_dist_group_spmv);
+                               halo moved with device-to-device copies; test harness */
+};
+enum { PJDS_NO_OVERLAP = 1u /* serialise exchange and compute (vector mode) */ };
+
+/*
+ * pjds_dist_create
+ *  plan          from pjds_dist_plan (not consumed; may be destroyed afterwards)
+ *  val_loc       host values of this rank's rows, in the CRS order given to pjds_dist_plan
+ *  send_counts   [nranks] entries this rank sends to each peer
+ *  send_cols     concatenation over peers (ascending rank) of GLOBAL column ids owned by this rank,
+ *                each peer's list in that peer's recv order (ascending)
+ *  transport     PJDS_TRANSPORT_*; nccl_unique_id used for NCCL when nranks > 1 (collective call)
+ *  block_rows    as pjds_create_from_crs
+ */
+int pjds_dist_create(pjds_dist_t* out, pjds_plan_t plan, const void* val_loc, int dtype,
+                     int32_t block_rows, const int64_t* send_counts, const int32_t* send_cols,
+                     int32_t transport, const void* nccl_unique_id);
+/* y_loc = A[rows of this rank, :] x ; x_loc / y_loc device pointers of length n_loc. */
+int pjds_dist_spmv(pjds_dist_t D, void* y_loc, const void* x_loc, void* stream, uint32_t flags);
+/* PJDS_TRANSPORT_LOCAL: one call runs all R ranks' spMVMs (same device allowed), D/y/x indexed by rank. */
+int pjds_dist_group_spmv(pjds_dist_t* D, int32_t nranks, void* const* y_loc, const void* const* x_loc,
+                         void* stream, uint32_t flags);
+typedef struct {
+  int64_t n_loc, halo, send_total, packed_send, rows_nonlocal;
+  int64_t nnz_local_part, nnz_nonlocal_part;
+  int32_t nranks, rank, peers_send, peers_recv, send_messages, recv_messages;
+} pjds_dist_info_t;
+int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* out);
+/* The two pJDS parts (owned by D; do not destroy): A_loc, A_nl (A_nl may be NULL if empty). */
+int pjds_dist_parts(pjds_dist_t D, pjds_t* A_loc, pjds_t* A_nl);
+int pjds_dist_destroy(pjds_dist_t D);
+
+/* NCCL helpers (NCCL is dlopen-ed; `libpath` NULL tries "libnccl.so.2"). */
+int pjds_nccl_load(const char* libpath);
+int pjds_nccl_unique_id(void* out128);
+
+/* ------------------------------------------------------------------ misc */
+
+/* Stream-bandwidth probe (roofline denominator, measured in the same run): copies / reads
+   `bytes` of device memory `reps` times; returns best GB/s of a copy (read+write bytes) and of a
+   read-only reduction.  Allocates and frees its own buffers. */
+int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs);
+
+/* Number of kernel launches this library has enqueued (process-wide counter). */
+int64_t pjds_launch_count(void);
+
+const char* pjds_last_error(void);
+const char* pjds_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PJDS_H */

@@ -1,0 +1,261 @@
+// C ABI of libpjds (include/pjds.h): single-GPU pJDS / ELLPACK-R handles.
+#include <cstring>
+#include <new>
+#include "internal.h"
+
+namespace pjds {
+
+static thread_local std::string g_err;
+int set_error(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+
+template <typename P>
+static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
+  *dst = nullptr;
+  if (bytes == 0) bytes = 16;  // keep a valid pointer for empty arrays
+  PJDS_CUDA_TRY(cudaMalloc((void**)dst, bytes));
+  if (src) PJDS_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return PJDS_OK;
+}
+
+int free_pjds_device(pjds_mat* A) {
+  cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
+  cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys);
+  A->d_val = A->d_xs = A->d_ys = nullptr;
+  A->d_col = A->d_block_len = A->d_perm = nullptr;
+  A->d_col_start = nullptr;
+  A->on_device = false;
+  return PJDS_OK;
+}
+
+// Upload the host arrays; the per-row store target is perm[k] (or store_map[perm[k]] when a
+// composition is requested, e.g. A_nl rows -> local rows).  Host val/col are released afterwards.
+int upload_pjds(pjds_mat* A, const int32_t* store_map) {
+  auto& h = A->h;
+  PJDS_CUDA_TRY(cudaGetDevice(&A->device));
+  std::vector<int32_t> target;
+  const int32_t* tp = h.perm.data();
+  if (store_map) {
+    target.resize(h.n);
+    for (int64_t k = 0; k < h.n; ++k) target[k] = store_map[h.perm[k]];
+    tp = target.data();
+  }
+  int s = PJDS_OK;
+  if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
+      (s = dmalloc_copy(&A->d_col, h.col.data(), h.col.size() * 4)) ||
+      (s = dmalloc_copy(&A->d_col_start, h.col_start.data(), h.col_start.size() * 8)) ||
+      (s = dmalloc_copy(&A->d_block_len, h.block_len.data(), h.block_len.size() * 4)) ||
+      (s = dmalloc_copy(&A->d_perm, tp, (size_t)h.n * 4))) {
+    free_pjds_device(A);
+    return s;
+  }
+  A->on_device = true;
+  std::vector<int32_t>().swap(h.col);
+  std::vector<uint8_t>().swap(h.val);
+  return PJDS_OK;
+}
+
+}  // namespace pjds
+
+using namespace pjds;
+
+extern "C" {
+
+const char* pjds_last_error(void) { return g_err.c_str(); }
+const char* pjds_version(void) { return "libpjds 0.1 (sm_100a)"; }
+
+int pjds_create_from_crs(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                         int dtype, int32_t block_rows, uint32_t flags) {
+  if (!out) return set_error(PJDS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (flags & ~(uint32_t)(PJDS_PERM_SYMMETRIC | PJDS_HOST_ONLY)) return set_error(PJDS_ERR_INVALID_ARG, "unknown flags");
+  if (block_rows == 0) block_rows = 32;
+  pjds_mat* A = new (std::nothrow) pjds_mat();
+  if (!A) return set_error(PJDS_ERR_OOM, "handle allocation failed");
+  A->flags = flags;
+  int s = convert_pjds(A->h, n, n, rowptr, col, val, dtype, block_rows, flags & PJDS_PERM_SYMMETRIC);
+  if (s == PJDS_OK && !(flags & PJDS_HOST_ONLY)) {
+    if (flags & PJDS_PERM_SYMMETRIC) {
+      // permuted basis: y_perm[k] is stored at k (identity store map)
+      std::vector<int32_t> ident(n);
+      for (int64_t k = 0; k < n; ++k) ident[A->h.perm[k]] = (int32_t)k;  // perm[k] -> k
+      s = upload_pjds(A, ident.data());
+    } else {
+      s = upload_pjds(A, nullptr);
+    }
+  }
+  if (s != PJDS_OK) {
+    delete A;
+    return s;
+  }
+  A->ncols = n;
+  *out = A;
+  return PJDS_OK;
+}
+
+int pjds_destroy(pjds_t A) {
+  if (!A) return PJDS_OK;
+  if (A->on_device) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (A->device >= 0) cudaSetDevice(A->device);
+    free_pjds_device(A);
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete A;
+  return PJDS_OK;
+}
+
+int pjds_spmv(pjds_t A, void* y, const void* x, void* stream) {
+  if (!A || !y || (!x && A->h.n > 0)) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: NULL argument");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: handle is host-only");
+  if (y == x) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: y aliases x");
+  return launch_pjds_spmv(A, y, x, (cudaStream_t)stream, false);
+}
+
+int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream) {
+  if (!A || !y_host || !x_host) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host: NULL argument");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host: handle is host-only");
+  const size_t bytes_x = (size_t)A->ncols * dtype_size(A->h.dtype), bytes_y = (size_t)A->h.n * dtype_size(A->h.dtype);
+  if (!A->d_xs) {
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_xs, bytes_x ? bytes_x : 16));
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_ys, bytes_y ? bytes_y : 16));
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  PJDS_CUDA_TRY(cudaMemcpyAsync(A->d_xs, x_host, bytes_x, cudaMemcpyHostToDevice, s));
+  PJDS_TRY(launch_pjds_spmv(A, A->d_ys, A->d_xs, s, false));
+  PJDS_CUDA_TRY(cudaMemcpyAsync(y_host, A->d_ys, bytes_y, cudaMemcpyDeviceToHost, s));
+  PJDS_CUDA_TRY(cudaStreamSynchronize(s));
+  return PJDS_OK;
+}
+
+int pjds_info(pjds_t A, pjds_info_t* o) {
+  if (!A || !o) return set_error(PJDS_ERR_INVALID_ARG, "pjds_info: NULL argument");
+  const auto& h = A->h;
+  std::memset(o, 0, sizeof(*o));
+  o->n = h.n; o->nnz = h.nnz; o->n_pad = h.n_pad; o->n_blocks = h.n_blocks; o->stored = h.stored;
+  o->block_rows = h.br; o->width = h.width; o->dtype = h.dtype; o->flags = (int32_t)A->flags;
+  o->len_min = h.len_min; o->len_max = h.len_max;
+  o->len_mean = h.n ? (double)h.nnz / (double)h.n : 0.0;
+  o->useful_fma = h.nnz;
+  o->padded_fma = h.stored - h.nnz;
+  o->idle_lane_slots = 0;
+  o->bytes_values = h.stored * (int64_t)dtype_size(h.dtype);
+  o->bytes_indices = h.stored * 4;
+  o->bytes_aux = (int64_t)(h.width + 1) * 8 + h.n_blocks * 4 + h.n * 4;
+  o->bytes_total = o->bytes_values + o->bytes_indices + o->bytes_aux;
+  const int64_t ell = (h.n + 31) / 32 * 32 * (int64_t)h.width;
+  o->data_reduction_vs_ellpack = ell ? 1.0 - (double)h.stored / (double)ell : 0.0;
+  o->on_device = A->on_device;
+  o->device = A->device;
+  return PJDS_OK;
+}
+
+int pjds_histogram(pjds_t A, int64_t* counts, int32_t nbins) {
+  if (!A || !counts || nbins < 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_histogram: bad argument");
+  for (int32_t L = 0; L < nbins; ++L) counts[L] = L < (int32_t)A->h.hist.size() ? A->h.hist[L] : 0;
+  return PJDS_OK;
+}
+
+int pjds_export(pjds_t A, int32_t* perm, int32_t* block_len, int64_t* col_start, int32_t* col, void* val) {
+  if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_export: NULL handle");
+  const auto& h = A->h;
+  if (perm) std::memcpy(perm, h.perm.data(), (size_t)h.n * 4);
+  if (block_len) std::memcpy(block_len, h.block_len.data(), (size_t)h.n_blocks * 4);
+  if (col_start) std::memcpy(col_start, h.col_start.data(), (size_t)(h.width + 1) * 8);
+  const size_t vb = (size_t)h.stored * dtype_size(h.dtype);
+  if (A->on_device) {
+    if (col) PJDS_CUDA_TRY(cudaMemcpy(col, A->d_col, (size_t)h.stored * 4, cudaMemcpyDeviceToHost));
+    if (val) PJDS_CUDA_TRY(cudaMemcpy(val, A->d_val, vb, cudaMemcpyDeviceToHost));
+  } else {
+    if (col) std::memcpy(col, h.col.data(), (size_t)h.stored * 4);
+    if (val) std::memcpy(val, h.val.data(), vb);
+  }
+  return PJDS_OK;
+}
+
+// ---- ELLPACK-R ------------------------------------------------------------------------------
+int ellr_create_from_crs(ellr_t* out, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                         int dtype, uint32_t flags) {
+  if (!out) return set_error(PJDS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (flags & ~(uint32_t)PJDS_HOST_ONLY) return set_error(PJDS_ERR_INVALID_ARG, "unknown flags");
+  ellr_mat* A = new (std::nothrow) ellr_mat();
+  if (!A) return set_error(PJDS_ERR_OOM, "handle allocation failed");
+  A->flags = flags;
+  int s = convert_ellr(A->h, n, rowptr, col, val, dtype);
+  if (s == PJDS_OK && !(flags & PJDS_HOST_ONLY)) {
+    auto& h = A->h;
+    cudaGetDevice(&A->device);
+    if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
+        (s = dmalloc_copy(&A->d_col, h.col.data(), h.col.size() * 4)) ||
+        (s = dmalloc_copy(&A->d_rowmax, h.rowmax.data(), h.rowmax.size() * 4))) {
+      cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_rowmax);
+    } else {
+      A->on_device = true;
+      std::vector<int32_t>().swap(h.col);
+      std::vector<uint8_t>().swap(h.val);
+    }
+  }
+  if (s != PJDS_OK) {
+    delete A;
+    return s;
+  }
+  *out = A;
+  return PJDS_OK;
+}
+
+int ellr_destroy(ellr_t A) {
+  if (!A) return PJDS_OK;
+  if (A->on_device) {
+    cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_rowmax);
+  }
+  delete A;
+  return PJDS_OK;
+}
+
+int ellr_spmv(ellr_t A, void* y, const void* x, void* stream) {
+  if (!A || !y || (!x && A->h.n > 0)) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: NULL argument");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: handle is host-only");
+  if (y == x) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: y aliases x");
+  return launch_ellr_spmv(A, y, x, (cudaStream_t)stream);
+}
+
+int ellr_info(ellr_t A, ellr_info_t* o) {
+  if (!A || !o) return set_error(PJDS_ERR_INVALID_ARG, "ellr_info: NULL argument");
+  const auto& h = A->h;
+  std::memset(o, 0, sizeof(*o));
+  o->n = h.n; o->nnz = h.nnz; o->n_pad = h.n_pad; o->stored = h.stored; o->width = h.width; o->dtype = h.dtype;
+  o->useful_fma = h.nnz; o->padded_fma = 0; o->idle_lane_slots = h.idle;
+  o->bytes_values = h.stored * (int64_t)dtype_size(h.dtype);
+  o->bytes_indices = h.stored * 4;
+  o->bytes_aux = h.n_pad * 4;
+  o->bytes_total = o->bytes_values + o->bytes_indices + o->bytes_aux;
+  o->on_device = A->on_device;
+  o->device = A->device;
+  return PJDS_OK;
+}
+
+int ellr_export(ellr_t A, int32_t* rowmax, int32_t* col, void* val) {
+  if (!A) return set_error(PJDS_ERR_INVALID_ARG, "ellr_export: NULL handle");
+  const auto& h = A->h;
+  if (rowmax) std::memcpy(rowmax, h.rowmax.data(), (size_t)h.n_pad * 4);
+  const size_t vb = (size_t)h.stored * dtype_size(h.dtype);
+  if (A->on_device) {
+    if (col) PJDS_CUDA_TRY(cudaMemcpy(col, A->d_col, (size_t)h.stored * 4, cudaMemcpyDeviceToHost));
+    if (val) PJDS_CUDA_TRY(cudaMemcpy(val, A->d_val, vb, cudaMemcpyDeviceToHost));
+  } else {
+    if (col) std::memcpy(col, h.col.data(), (size_t)h.stored * 4);
+    if (val) std::memcpy(val, h.val.data(), vb);
+  }
+  return PJDS_OK;
+}
+
+int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs) {
+  if (!copy_gbs || !read_gbs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_bw_probe: NULL argument");
+  return bw_probe(bytes, reps, copy_gbs, read_gbs);
+}
+
+}  // extern "C"

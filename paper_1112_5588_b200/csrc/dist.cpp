@@ -1,0 +1,522 @@
+// Row-partitioned distributed spMVM (§3) over NCCL point-to-point.
+//
+//   plan    : split of this rank's rows into a local part (owned columns) and a nonlocal part
+//             (columns owned by other ranks); recv lists per owner
+//             (sorted unique global ids) and halo slots (position in the owner-ordered
+//             concatenation).
+//   create  : A_loc (all rows, local column ids) and A_nl (rows with >= 1 nonlocal entry,
+//             halo-slot column ids) as pJDS; send schedule from the caller-exchanged lists.
+//             A peer's list whose entries form at most kMaxRuns contiguous runs is sent straight
+//             from x (one message per run, no pack); otherwise it is packed ("local gather",
+//             Fig. 4 caption L401-402) into a contiguous buffer by a kernel.  Sender and receiver
+//             apply the same rule to the same list, so message boundaries always match.
+//   spmv    : task mode (L454-461) with a CUDA stream as the dedicated communication context:
+//               comm stream (high priority): [pack] -> ncclGroupStart/Send/Recv/ncclGroupEnd
+//               compute stream             : A_loc kernel (y = ...)      -- overlapped
+//               compute stream             : wait(comm) -> A_nl kernel (y += ..., written twice, L445)
+//             PJDS_NO_OVERLAP serialises everything on the compute stream (vector mode, L437-440).
+#include <algorithm>
+#include <cstring>
+#include <dlfcn.h>
+#include <mutex>
+#include <new>
+#include <omp.h>
+#include "internal.h"
+#include "nccl.h"
+
+using namespace pjds;
+
+struct pjds_plan {
+  int32_t R = 1, rank = 0;
+  int64_t n_global = 0, lo = 0, hi = 0, n_loc = 0, nnz_loc = 0;
+  std::vector<int64_t> offsets;
+  std::vector<int64_t> loc_rowptr, loc_src;  // local part: CRS with local column ids
+  std::vector<int32_t> loc_col;
+  std::vector<int64_t> nl_rowptr, nl_src;    // nonlocal part: CRS with halo-slot column ids
+  std::vector<int32_t> nl_col, rows_nl;
+  std::vector<int64_t> recv_counts;          // [R]
+  std::vector<int32_t> recv_cols;            // [halo] global ids, owner-ordered
+};
+
+namespace {
+
+constexpr int kMaxRuns = 64;
+
+// ---- NCCL (dlopen) ------------------------------------------------------------------------
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+int nccl_load(const char* path) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.h) return PJDS_OK;
+  const char* names[] = {path, "libnccl.so.2", "libnccl.so"};
+  void* h = nullptr;
+  for (const char* nm : names) {
+    if (!nm) continue;
+    h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (h) break;
+  }
+  if (!h) return set_error(PJDS_ERR_NCCL, std::string("cannot dlopen NCCL: ") + dlerror());
+  Nccl n;
+  n.h = h;
+#define SYM(field, name)                                                            \
+  n.field = (decltype(n.field))dlsym(h, name);                                      \
+  if (!n.field) return set_error(PJDS_ERR_NCCL, std::string("NCCL symbol missing: ") + name);
+  SYM(getUniqueId, "ncclGetUniqueId");
+  SYM(commInitRank, "ncclCommInitRank");
+  SYM(commDestroy, "ncclCommDestroy");
+  SYM(send, "ncclSend");
+  SYM(recv, "ncclRecv");
+  SYM(groupStart, "ncclGroupStart");
+  SYM(groupEnd, "ncclGroupEnd");
+  SYM(errStr, "ncclGetErrorString");
+#undef SYM
+  g_nccl = n;
+  return PJDS_OK;
+}
+
+#define NCCL_TRY(expr)                                                                        \
+  do {                                                                                        \
+    ncclResult_t _r = (expr);                                                                 \
+    if (_r != ncclSuccess) return set_error(PJDS_ERR_NCCL, std::string(#expr) + ": " + g_nccl.errStr(_r)); \
+  } while (0)
+
+ncclDataType_t nccl_type(int dt) { return dt == PJDS_F64 ? ncclFloat64 : ncclFloat32; }
+
+struct Run {
+  int64_t src;    // sender: local index in x (direct) ; receiver: unused
+  int64_t dst;    // offset in the peer's message space (halo slot / packed offset)
+  int64_t count;
+};
+
+// runs of consecutive values in ids[0..m)
+std::vector<std::pair<int64_t, int64_t>> runs_of(const int32_t* ids, int64_t m) {
+  std::vector<std::pair<int64_t, int64_t>> r;  // (first value, length)
+  for (int64_t i = 0; i < m;) {
+    int64_t j = i + 1;
+    while (j < m && ids[j] == ids[j - 1] + 1) ++j;
+    r.push_back({ids[i], j - i});
+    i = j;
+  }
+  return r;
+}
+
+}  // namespace
+
+struct pjds_dist {
+  int32_t R = 1, rank = 0, transport = PJDS_TRANSPORT_NCCL, dtype = PJDS_F64, device = 0;
+  int64_t n_loc = 0, halo = 0, send_total = 0, packed_total = 0;
+  int64_t nnz_loc_part = 0, nnz_nl_part = 0, rows_nl = 0;
+  pjds_mat* A_loc = nullptr;
+  pjds_mat* A_nl = nullptr;
+  // send side
+  struct PeerSend {
+    int32_t peer;
+    bool packed;
+    std::vector<std::pair<int64_t, int64_t>> runs;  // direct: (x_loc offset, count); packed: one (packbuf offset, count)
+  };
+  std::vector<PeerSend> sends;
+  std::vector<int32_t> pack_idx_host;  // local ids for the pack kernel
+  int32_t* d_pack_idx = nullptr;
+  void* d_packbuf = nullptr;
+  // recv side
+  struct PeerRecv {
+    int32_t peer;
+    std::vector<std::pair<int64_t, int64_t>> runs;  // (halo offset, count), one per message
+  };
+  std::vector<PeerRecv> recvs;
+  std::vector<int64_t> recv_counts;
+  void* d_halo = nullptr;
+  // streams / events
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
+  ncclComm_t nccl = nullptr;
+  int send_messages = 0, recv_messages = 0;
+};
+
+namespace {
+
+size_t vsz(const pjds_dist* D) { return dtype_size(D->dtype); }
+
+// Enqueue this rank's sends and receives (NCCL transport) on `s`.
+int post_nccl(pjds_dist* D, const void* x_loc, cudaStream_t s) {
+  const size_t vs = vsz(D);
+  NCCL_TRY(g_nccl.groupStart());
+  for (auto& ps : D->sends) {
+    const char* base = ps.packed ? (const char*)D->d_packbuf : (const char*)x_loc;
+    for (auto& r : ps.runs)
+      NCCL_TRY(g_nccl.send(base + r.first * vs, (size_t)r.second, nccl_type(D->dtype), ps.peer, D->nccl, s));
+  }
+  for (auto& pr : D->recvs)
+    for (auto& r : pr.runs)
+      NCCL_TRY(g_nccl.recv((char*)D->d_halo + r.first * vs, (size_t)r.second, nccl_type(D->dtype), pr.peer, D->nccl, s));
+  NCCL_TRY(g_nccl.groupEnd());
+  return PJDS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pjds_nccl_load(const char* libpath) { return nccl_load(libpath); }
+
+int pjds_nccl_unique_id(void* out128) {
+  if (!out128) return set_error(PJDS_ERR_INVALID_ARG, "pjds_nccl_unique_id: NULL");
+  PJDS_TRY(nccl_load(nullptr));
+  ncclUniqueId id;
+  NCCL_TRY(g_nccl.getUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return PJDS_OK;
+}
+
+int pjds_dist_plan(pjds_plan_t* out, int32_t R, int32_t rank, int64_t n_global, const int64_t* offs,
+                   const int64_t* rowptr, const int32_t* col) {
+  if (!out || !offs || !rowptr) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_plan: NULL argument");
+  *out = nullptr;
+  if (R < 1 || rank < 0 || rank >= R) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_plan: bad nranks/rank");
+  if (offs[0] != 0 || offs[R] != n_global) return set_error(PJDS_ERR_INVALID_ARG, "row_offsets must span [0, n_global]");
+  for (int q = 0; q < R; ++q)
+    if (offs[q + 1] < offs[q]) return set_error(PJDS_ERR_INVALID_ARG, "row_offsets must be non-decreasing");
+  const int64_t lo = offs[rank], hi = offs[rank + 1], nl = hi - lo;
+  PJDS_TRY(validate_crs(nl, n_global, rowptr, col));
+  pjds_plan* P = new (std::nothrow) pjds_plan();
+  if (!P) return set_error(PJDS_ERR_OOM, "plan allocation failed");
+  try {
+    P->R = R; P->rank = rank; P->n_global = n_global; P->lo = lo; P->hi = hi; P->n_loc = nl;
+    P->offsets.assign(offs, offs + R + 1);
+    const int64_t nnz = rowptr[nl];
+    P->nnz_loc = nnz;
+    // mark remote columns, then the owner-ordered sorted unique list == ascending global ids
+    std::vector<uint8_t> mark(n_global, 0);
+#pragma omp parallel for
+    for (int64_t k = 0; k < nnz; ++k) {
+      int64_t c = col[k];
+      if (c < lo || c >= hi) mark[c] = 1;
+    }
+    for (int64_t c = 0; c < n_global; ++c)
+      if (mark[c]) P->recv_cols.push_back((int32_t)c);
+    P->recv_counts.assign(R, 0);
+    for (int32_t c : P->recv_cols) {
+      int q = (int)(std::upper_bound(offs, offs + R + 1, (int64_t)c) - offs) - 1;
+      P->recv_counts[q]++;
+    }
+    // split rows
+    std::vector<int32_t> loc_len(nl), nl_len(nl);
+#pragma omp parallel for
+    for (int64_t i = 0; i < nl; ++i) {
+      int32_t a = 0, b = 0;
+      for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+        if (col[k] >= lo && col[k] < hi) ++a;
+        else ++b;
+      }
+      loc_len[i] = a;
+      nl_len[i] = b;
+    }
+    P->loc_rowptr.assign(nl + 1, 0);
+    for (int64_t i = 0; i < nl; ++i) {
+      P->loc_rowptr[i + 1] = P->loc_rowptr[i] + loc_len[i];
+      if (nl_len[i]) P->rows_nl.push_back((int32_t)i);
+    }
+    const int64_t m = (int64_t)P->rows_nl.size();
+    P->nl_rowptr.assign(m + 1, 0);
+    for (int64_t a = 0; a < m; ++a) P->nl_rowptr[a + 1] = P->nl_rowptr[a] + nl_len[P->rows_nl[a]];
+    P->loc_col.resize(P->loc_rowptr[nl]);
+    P->loc_src.resize(P->loc_rowptr[nl]);
+    P->nl_col.resize(P->nl_rowptr[m]);
+    P->nl_src.resize(P->nl_rowptr[m]);
+    std::vector<int64_t> nl_pos(nl, -1);
+    for (int64_t a = 0; a < m; ++a) nl_pos[P->rows_nl[a]] = P->nl_rowptr[a];
+    const int32_t* rc = P->recv_cols.data();
+    const int64_t h = (int64_t)P->recv_cols.size();
+#pragma omp parallel for
+    for (int64_t i = 0; i < nl; ++i) {
+      int64_t pl = P->loc_rowptr[i], pn = nl_pos[i];
+      for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+        const int32_t c = col[k];
+        if (c >= lo && c < hi) {
+          P->loc_col[pl] = (int32_t)(c - lo);
+          P->loc_src[pl++] = k;
+        } else {
+          P->nl_col[pn] = (int32_t)(std::lower_bound(rc, rc + h, c) - rc);
+          P->nl_src[pn++] = k;
+        }
+      }
+    }
+  } catch (const std::bad_alloc&) {
+    delete P;
+    return set_error(PJDS_ERR_OOM, "host allocation failed in pjds_dist_plan");
+  }
+  *out = P;
+  return PJDS_OK;
+}
+
+int pjds_dist_plan_info(pjds_plan_t P, pjds_plan_info_t* o) {
+  if (!P || !o) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_plan_info: NULL argument");
+  std::memset(o, 0, sizeof(*o));
+  o->n_loc = P->n_loc; o->nnz_loc = P->nnz_loc;
+  o->nnz_local_part = (int64_t)P->loc_col.size();
+  o->nnz_nonlocal_part = (int64_t)P->nl_col.size();
+  o->rows_nonlocal = (int64_t)P->rows_nl.size();
+  o->halo = (int64_t)P->recv_cols.size();
+  o->nranks = P->R; o->rank = P->rank;
+  return PJDS_OK;
+}
+
+int pjds_dist_plan_recv(pjds_plan_t P, int64_t* counts, int32_t* cols) {
+  if (!P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_plan_recv: NULL plan");
+  if (counts) std::memcpy(counts, P->recv_counts.data(), P->recv_counts.size() * 8);
+  if (cols) std::memcpy(cols, P->recv_cols.data(), P->recv_cols.size() * 4);
+  return PJDS_OK;
+}
+
+int pjds_dist_plan_destroy(pjds_plan_t P) {
+  delete P;
+  return PJDS_OK;
+}
+
+int pjds_dist_destroy(pjds_dist_t D);
+
+int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype, int32_t block_rows,
+                     const int64_t* send_counts, const int32_t* send_cols, int32_t transport, const void* nccl_id) {
+  if (!out || !P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: NULL argument");
+  *out = nullptr;
+  if (dtype != PJDS_F32 && dtype != PJDS_F64) return set_error(PJDS_ERR_INVALID_ARG, "bad dtype");
+  if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL)
+    return set_error(PJDS_ERR_INVALID_ARG, "bad transport");
+  if (P->nnz_loc > 0 && !val) return set_error(PJDS_ERR_INVALID_ARG, "val is NULL");
+  if (P->R > 1 && !send_counts) return set_error(PJDS_ERR_INVALID_ARG, "send_counts is NULL");
+  if (block_rows == 0) block_rows = 32;
+  const int R = P->R;
+  int64_t send_total = 0;
+  for (int q = 0; q < R && send_counts; ++q) {
+    if (send_counts[q] < 0) return set_error(PJDS_ERR_INVALID_ARG, "negative send count");
+    if (q == P->rank && send_counts[q] != 0) return set_error(PJDS_ERR_INVALID_ARG, "send to self");
+    send_total += send_counts[q];
+  }
+  if (send_total > 0 && !send_cols) return set_error(PJDS_ERR_INVALID_ARG, "send_cols is NULL");
+  for (int64_t i = 0; i < send_total; ++i)
+    if (send_cols[i] < P->lo || send_cols[i] >= P->hi)
+      return set_error(PJDS_ERR_INVALID_ARG, "send_cols entry not owned by this rank");
+
+  pjds_dist* D = new (std::nothrow) pjds_dist();
+  if (!D) return set_error(PJDS_ERR_OOM, "dist allocation failed");
+  D->R = R; D->rank = P->rank; D->transport = transport; D->dtype = dtype;
+  D->n_loc = P->n_loc; D->halo = (int64_t)P->recv_cols.size(); D->send_total = send_total;
+  D->nnz_loc_part = (int64_t)P->loc_col.size(); D->nnz_nl_part = (int64_t)P->nl_col.size();
+  D->rows_nl = (int64_t)P->rows_nl.size();
+  D->recv_counts = P->recv_counts;
+  cudaGetDevice(&D->device);
+  const size_t vs = dtype_size(dtype);
+  int s = PJDS_OK;
+  auto fail = [&](int st) { pjds_dist_destroy(D); return st; };
+  try {
+    // ---- the two pJDS parts
+    std::vector<uint8_t> v_loc(P->loc_src.size() * vs), v_nl(P->nl_src.size() * vs);
+    const uint8_t* vin = (const uint8_t*)val;
+    for (size_t k = 0; k < P->loc_src.size(); ++k) std::memcpy(&v_loc[k * vs], vin + P->loc_src[k] * vs, vs);
+    for (size_t k = 0; k < P->nl_src.size(); ++k) std::memcpy(&v_nl[k * vs], vin + P->nl_src[k] * vs, vs);
+    D->A_loc = new pjds_mat();
+    s = convert_pjds(D->A_loc->h, P->n_loc, P->n_loc, P->loc_rowptr.data(), P->loc_col.data(), v_loc.data(), dtype,
+                     block_rows, false);
+    if (s == PJDS_OK) s = upload_pjds(D->A_loc, nullptr);
+    if (s != PJDS_OK) return fail(s);
+    D->A_loc->ncols = P->n_loc;
+    const int64_t m = (int64_t)P->rows_nl.size();
+    if (m > 0) {
+      D->A_nl = new pjds_mat();
+      s = convert_pjds(D->A_nl->h, m, std::max<int64_t>(D->halo, 1), P->nl_rowptr.data(), P->nl_col.data(),
+                       v_nl.data(), dtype, block_rows, false);
+      if (s == PJDS_OK) s = upload_pjds(D->A_nl, P->rows_nl.data());  // store to local row rows_nl[perm[k]]
+      if (s != PJDS_OK) return fail(s);
+      D->A_nl->ncols = D->halo;
+    }
+    // ---- send schedule
+    int64_t pos = 0;
+    for (int q = 0; q < R && send_counts; ++q) {
+      const int64_t cnt = send_counts[q];
+      if (!cnt) continue;
+      std::vector<int32_t> ids(cnt);
+      for (int64_t i = 0; i < cnt; ++i) ids[i] = (int32_t)(send_cols[pos + i] - P->lo);
+      pos += cnt;
+      auto runs = runs_of(ids.data(), cnt);
+      pjds_dist::PeerSend ps;
+      ps.peer = q;
+      if ((int)runs.size() <= kMaxRuns) {
+        ps.packed = false;
+        ps.runs = runs;
+      } else {
+        ps.packed = true;
+        ps.runs = {{D->packed_total, cnt}};
+        D->pack_idx_host.insert(D->pack_idx_host.end(), ids.begin(), ids.end());
+        D->packed_total += cnt;
+      }
+      D->send_messages += (int)ps.runs.size();
+      D->sends.push_back(std::move(ps));
+    }
+    // ---- recv schedule (same run rule on the same lists)
+    int64_t hoff = 0;
+    for (int q = 0; q < R; ++q) {
+      const int64_t cnt = P->recv_counts[q];
+      if (!cnt) continue;
+      auto runs = runs_of(P->recv_cols.data() + hoff, cnt);
+      pjds_dist::PeerRecv pr;
+      pr.peer = q;
+      if ((int)runs.size() <= kMaxRuns) {
+        int64_t o = hoff;
+        for (auto& r : runs) {
+          pr.runs.push_back({o, r.second});
+          o += r.second;
+        }
+      } else {
+        pr.runs = {{hoff, cnt}};
+      }
+      D->recv_messages += (int)pr.runs.size();
+      D->recvs.push_back(std::move(pr));
+      hoff += cnt;
+    }
+  } catch (const std::bad_alloc&) {
+    return fail(set_error(PJDS_ERR_OOM, "host allocation failed in pjds_dist_create"));
+  }
+  // ---- device buffers, streams, transport
+  if (cudaMalloc(&D->d_halo, std::max<size_t>(D->halo * vs, 16)) != cudaSuccess)
+    return fail(set_error(PJDS_ERR_OOM, "halo allocation failed"));
+  if (D->packed_total) {
+    if (cudaMalloc(&D->d_packbuf, D->packed_total * vs) != cudaSuccess ||
+        cudaMalloc(&D->d_pack_idx, D->packed_total * 4) != cudaSuccess)
+      return fail(set_error(PJDS_ERR_OOM, "pack buffer allocation failed"));
+    if (cudaMemcpy(D->d_pack_idx, D->pack_idx_host.data(), D->packed_total * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(set_error(PJDS_ERR_CUDA, "pack index upload failed"));
+  }
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  if (cudaStreamCreateWithPriority(&D->comm, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
+      cudaEventCreateWithFlags(&D->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&D->ev_comm, cudaEventDisableTiming) != cudaSuccess)
+    return fail(set_error(PJDS_ERR_CUDA, "stream/event creation failed"));
+  if (transport == PJDS_TRANSPORT_NCCL && R > 1) {
+    if (!nccl_id) return fail(set_error(PJDS_ERR_INVALID_ARG, "nccl_unique_id is NULL"));
+    if ((s = nccl_load(nullptr)) != PJDS_OK) return fail(s);
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = g_nccl.commInitRank(&D->nccl, R, id, P->rank);
+    if (r != ncclSuccess) return fail(set_error(PJDS_ERR_NCCL, std::string("ncclCommInitRank: ") + g_nccl.errStr(r)));
+  }
+  *out = D;
+  return PJDS_OK;
+}
+
+int pjds_dist_destroy(pjds_dist_t D) {
+  if (!D) return PJDS_OK;
+  if (D->nccl && g_nccl.commDestroy) g_nccl.commDestroy(D->nccl);
+  if (D->comm) cudaStreamDestroy(D->comm);
+  if (D->ev_ready) cudaEventDestroy(D->ev_ready);
+  if (D->ev_comm) cudaEventDestroy(D->ev_comm);
+  cudaFree(D->d_halo); cudaFree(D->d_packbuf); cudaFree(D->d_pack_idx);
+  pjds_destroy(D->A_loc);
+  pjds_destroy(D->A_nl);
+  delete D;
+  return PJDS_OK;
+}
+
+int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* o) {
+  if (!D || !o) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_info: NULL argument");
+  std::memset(o, 0, sizeof(*o));
+  o->n_loc = D->n_loc; o->halo = D->halo; o->send_total = D->send_total; o->packed_send = D->packed_total;
+  o->rows_nonlocal = D->rows_nl; o->nnz_local_part = D->nnz_loc_part; o->nnz_nonlocal_part = D->nnz_nl_part;
+  o->nranks = D->R; o->rank = D->rank;
+  o->peers_send = (int32_t)D->sends.size(); o->peers_recv = (int32_t)D->recvs.size();
+  o->send_messages = D->send_messages; o->recv_messages = D->recv_messages;
+  return PJDS_OK;
+}
+
+int pjds_dist_parts(pjds_dist_t D, pjds_t* a, pjds_t* b) {
+  if (!D) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_parts: NULL");
+  if (a) *a = D->A_loc;
+  if (b) *b = D->A_nl;
+  return PJDS_OK;
+}
+
+int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t flags) {
+  if (!D || (D->n_loc > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: NULL argument");
+  if (y == x && D->n_loc > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: y aliases x");
+  if (D->transport != PJDS_TRANSPORT_NCCL) return set_error(PJDS_ERR_INVALID_ARG, "use pjds_dist_group_spmv for LOCAL transport");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool comm_needed = D->R > 1 && (!D->sends.empty() || !D->recvs.empty());
+  if (!comm_needed) {  // R = 1 or no halo: local part only (+ empty nonlocal)
+    PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+    return PJDS_OK;
+  }
+  if (flags & PJDS_NO_OVERLAP) {
+    if (D->packed_total) PJDS_TRY(launch_pack(D->d_pack_idx, D->packed_total, x, D->d_packbuf, D->dtype, s));
+    PJDS_TRY(post_nccl(D, x, s));
+    PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+    if (D->A_nl) PJDS_TRY(launch_pjds_spmv(D->A_nl, y, D->d_halo, s, true));
+    return PJDS_OK;
+  }
+  // task mode: comm stream starts after x is ready on the compute stream
+  PJDS_CUDA_TRY(cudaEventRecord(D->ev_ready, s));
+  PJDS_CUDA_TRY(cudaStreamWaitEvent(D->comm, D->ev_ready, 0));
+  if (D->packed_total) PJDS_TRY(launch_pack(D->d_pack_idx, D->packed_total, x, D->d_packbuf, D->dtype, D->comm));
+  PJDS_TRY(post_nccl(D, x, D->comm));
+  PJDS_CUDA_TRY(cudaEventRecord(D->ev_comm, D->comm));
+  PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+  PJDS_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_comm, 0));
+  if (D->A_nl) PJDS_TRY(launch_pjds_spmv(D->A_nl, y, D->d_halo, s, true));
+  return PJDS_OK;
+}
+
+int pjds_dist_group_spmv(pjds_dist_t* Ds, int32_t R, void* const* y, const void* const* x, void* stream,
+                         uint32_t flags) {
+  (void)flags;
+  if (!Ds || R < 1 || !y || !x) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_group_spmv: bad argument");
+  for (int r = 0; r < R; ++r)
+    if (!Ds[r] || Ds[r]->R != R || Ds[r]->rank != r || Ds[r]->transport != PJDS_TRANSPORT_LOCAL)
+      return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_group_spmv: handles must be LOCAL, rank-ordered, same R");
+  cudaStream_t s = (cudaStream_t)stream;
+  // 1. pack (local gather) on every rank
+  for (int r = 0; r < R; ++r) {
+    pjds_dist* D = Ds[r];
+    if (D->packed_total) PJDS_TRY(launch_pack(D->d_pack_idx, D->packed_total, x[r], D->d_packbuf, D->dtype, s));
+  }
+  // 2. exchange: receiver r's message list from peer q matches sender q's list to r one-to-one
+  for (int r = 0; r < R; ++r) {
+    pjds_dist* D = Ds[r];
+    const size_t vs = vsz(D);
+    for (auto& pr : D->recvs) {
+      pjds_dist* S = Ds[pr.peer];
+      const pjds_dist::PeerSend* ps = nullptr;
+      for (auto& c : S->sends)
+        if (c.peer == r) ps = &c;
+      if (!ps || ps->runs.size() != pr.runs.size())
+        return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_group_spmv: send/recv schedules do not match");
+      const char* base = ps->packed ? (const char*)S->d_packbuf : (const char*)x[pr.peer];
+      for (size_t i = 0; i < pr.runs.size(); ++i) {
+        if (ps->runs[i].second != pr.runs[i].second)
+          return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_group_spmv: message sizes do not match");
+        PJDS_CUDA_TRY(cudaMemcpyAsync((char*)D->d_halo + pr.runs[i].first * vs, base + ps->runs[i].first * vs,
+                                      pr.runs[i].second * vs, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  // 3. local then nonlocal part on every rank
+  for (int r = 0; r < R; ++r) {
+    pjds_dist* D = Ds[r];
+    PJDS_TRY(launch_pjds_spmv(D->A_loc, y[r], x[r], s, false));
+    if (D->A_nl) PJDS_TRY(launch_pjds_spmv(D->A_nl, y[r], D->d_halo, s, true));
+  }
+  return PJDS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal declarations shared by the libpjds translation units (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "pjds.h"
+
+namespace pjds {
+
+// ---- errors -------------------------------------------------------------------------------
+int set_error(int status, const std::string& msg);
+inline int ok() { return PJDS_OK; }
+#define PJDS_CUDA_TRY(expr)                                                                   \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return ::pjds::set_error(_e == cudaErrorMemoryAllocation ? PJDS_ERR_OOM : PJDS_ERR_CUDA, \
+                               std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+  } while (0)
+#define PJDS_TRY(expr)          \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != PJDS_OK) return _s; \
+  } while (0)
+
+inline size_t dtype_size(int dt) { return dt == PJDS_F64 ? 8 : 4; }
+
+// ---- host-side pJDS arrays (conversion result) ---------------------------------------------
+struct PjdsHost {
+  int64_t n = 0, ncols = 0, nnz = 0, n_pad = 0, n_blocks = 0, stored = 0;
+  int32_t br = 32, width = 0, dtype = PJDS_F64, len_min = 0, len_max = 0;
+  std::vector<int32_t> perm;       // [n]  perm[new] = old
+  std::vector<int32_t> block_len;  // [n_blocks]
+  std::vector<int64_t> col_start;  // [width+1]
+  std::vector<int32_t> col;        // [stored]
+  std::vector<uint8_t> val;        // [stored * dtype_size]
+  std::vector<int64_t> hist;       // [len_max+1]
+};
+
+// CRS (rows x ncols) -> pJDS host arrays.  `val_src` optional gather index (val[k] = val_in[src[k]]).
+// Validates CRS; cols must be < ncols.  symmetric: columns -> invperm[col] (requires ncols == n).
+int convert_pjds(PjdsHost& out, int64_t n, int64_t ncols, const int64_t* rowptr, const int32_t* col,
+                 const void* val, int dtype, int32_t br, bool symmetric);
+
+struct EllrHost {
+  int64_t n = 0, nnz = 0, n_pad = 0, stored = 0, idle = 0;
+  int32_t width = 0, dtype = PJDS_F64;
+  std::vector<int32_t> rowmax, col;
+  std::vector<uint8_t> val;
+};
+int convert_ellr(EllrHost& out, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                 int dtype);
+
+int validate_crs(int64_t n, int64_t ncols, const int64_t* rowptr, const int32_t* col);
+
+}  // namespace pjds
+
+// ---- handles --------------------------------------------------------------------------------
+struct pjds_mat {
+  pjds::PjdsHost h;  // arrays are cleared (vectors freed) after upload unless host-only
+  uint32_t flags = 0;
+  bool on_device = false;
+  int device = -1;
+  void* d_val = nullptr;
+  int32_t* d_col = nullptr;
+  int64_t* d_col_start = nullptr;
+  int32_t* d_block_len = nullptr;
+  int32_t* d_perm = nullptr;  // store target per sorted row (orig row; or local row for A_nl)
+  void* d_xs = nullptr;       // staging for pjds_spmv_host
+  void* d_ys = nullptr;
+  int64_t ncols = 0;
+};
+
+struct ellr_mat {
+  pjds::EllrHost h;
+  uint32_t flags = 0;
+  bool on_device = false;
+  int device = -1;
+  void* d_val = nullptr;
+  int32_t* d_col = nullptr;
+  int32_t* d_rowmax = nullptr;
+};
+
+namespace pjds {
+int upload_pjds(pjds_mat* A, const int32_t* store_map /* optional: perm composed with this */);
+int free_pjds_device(pjds_mat* A);
+
+// ---- kernel launchers (kernels.cu) -----------------------------------------------------------
+int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool accumulate);
+int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s);
+int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int dtype, cudaStream_t s);
+int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
+void count_launch(int64_t k = 1);
+}  // namespace pjds
