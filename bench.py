@@ -8,6 +8,13 @@ Holstein-Hubbard matrix, M = 25 phonons, N = 57,002,400, nnz = 942,439,680, DP, 
 (inputs/gen.cpp), the same matrix for every N (strong scaling, rows partitioned on e-block
 boundaries of the nested spin-grid ordering).
 
+At N=1 the product runs in the permuted basis (PJDS_PERM_SYMMETRIC), the paper's usage for
+iterative solvers: "permutation of the indices needs to be done only before the start and after
+the end of the algorithm, while the complete iterative scheme works on the permuted elements"
+(PAPER.md L241-246); x is permuted once before the timed region (--basis rows: y stored through
+perm every step instead).  The rows-only pJDS and ELLPACK-R kernels are timed beside it
+("compare").  e2e includes the basis change on the GPU, both ways, every step.
+
   python bench.py [--gpus N --steps K --warmup W] [--config C5] [--dtype f64|f32] [--impl pjds|ellr|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
 
@@ -49,9 +56,11 @@ def parse():
     p.add_argument("--impl", default="pjds", choices=["pjds", "ellr", "reference"])
     p.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    p.add_argument("--basis", default="permuted", choices=["permuted", "rows"])
     p.add_argument("--block-rows", type=int, default=32)
     p.add_argument("--no-overlap", action="store_true", help="dist: vector mode (exchange, then compute)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-compare", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
     return p.parse_args()
@@ -114,29 +123,20 @@ def measured_peaks():
         return {}
 
 
-# ------------------------------------------------------------------------------------------ CPU baseline
-def cpu_baseline(cfg: str, npdt, budget_s: float = 12.0):
-    """The oracle's plain CRS loop (oracle_spmv_crs, OpenMP static over rows, all visible cores) on a
-    bounded sample of the workload: a leading row block of the matrix, repeated until ~budget_s."""
-    import inputs
+# ------------------------------------------------------------------------------------------ CPU oracle
+def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1):
+    """The oracle's plain CRS loop (oracle_spmv_crs: OpenMP static over rows, all visible cores),
+    repeated until the time budget is spent.  Returns (median seconds per product, reps, cores)."""
     import oracle
-    g = inputs.Generator.from_config(cfg)
-    rows = min(g.n, 4_000_000)
-    rp, col, val = g.crs(0, rows, dtype=npdt)
-    x = inputs.vector(g.n, npdt)
     cores = len(os.sched_getaffinity(0))
-    nnz = int(rp[-1])
-    oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)  # warm-up
+    oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)  # warm-up
     ts = []
     t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end and len(ts) < 50:
+    while (time.perf_counter() < t_end and len(ts) < max_reps) or len(ts) < min_reps:
         t0 = time.perf_counter()
-        oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)
+        oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)
         ts.append(time.perf_counter() - t0)
-    t = float(np.median(ts))
-    return {"value": 2.0 * nnz / t / 1e9, "unit": "GFlop/s", "cores": cores, "kind": "oracle",
-            "sample": f"rows [0,{rows}) of {cfg} ({nnz} nnz), {len(ts)} reps, median, "
-                      f"{sum(ts):.1f} s CPU time, oracle_spmv_crs {np.dtype(npdt).name}"}
+    return float(np.median(ts)), len(ts), cores, float(sum(ts))
 
 
 # ------------------------------------------------------------------------------------------ main
@@ -178,41 +178,49 @@ def main():
     lo, hi = int(offs[rank]), int(offs[rank + 1])
     rp, col, val = g.crs(lo, hi, dtype=npdt)
     nnz_loc = int(rp[-1])
+    x_host = inputs.vector(hi - lo, npdt, i0=lo)
+    permuted = world == 1 and a.impl == "pjds" and a.basis == "permuted"
+    compare = {}
+    footprint = None
     if world > 1:
         D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows)
-        A_loc, A_nl = D.parts()
-        stats = {"local_part": A_loc.info, "nonlocal_part": A_nl.info if A_nl else None, "dist": D.info}
         A = None
     else:
         if a.impl == "ellr":
             A = pj.EllrMatrix.from_crs(n, rp, col, val)
         else:
-            A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows)
-        stats = A.info
-    # footprint comparison (host-side accounting of both formats, bytes vs ELLPACK-R)
-    footprint = None
-    if world == 1:
-        if a.impl == "pjds":
-            ell_entries = (n + 31) // 32 * 32 * stats["len_max"]
-            footprint = {"pjds_bytes": stats["bytes_total"], "pjds_stored": stats["stored"],
-                         "ellr_bytes": ell_entries * (sv + 4) + (n + 31) // 32 * 32 * 4, "ellr_stored": ell_entries,
-                         "data_reduction_vs_ellpack": stats["data_reduction_vs_ellpack"]}
-            footprint["bytes_ratio_pjds_over_ellr"] = footprint["pjds_bytes"] / footprint["ellr_bytes"]
-    del col, val
+            A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows, symmetric=permuted)
+            st = A.info
+            ell_rows = (n + 31) // 32 * 32
+            ell_entries = ell_rows * st["len_max"]
+            footprint = {"pjds_bytes": st["bytes_total"], "pjds_stored": st["stored"],
+                         "ellr_bytes": ell_entries * (sv + 4) + ell_rows * 4, "ellr_stored": ell_entries,
+                         "data_reduction_vs_ellpack": round(st["data_reduction_vs_ellpack"], 5),
+                         "padding_entries": st["stored"] - st["nnz"]}
+            footprint["bytes_ratio_pjds_over_ellr"] = round(footprint["pjds_bytes"] / footprint["ellr_bytes"], 4)
+    # CPU oracle baseline on the same matrix (rank 0, N=1 only), bounded to ~10 s
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        t, reps, cores, tot = time_oracle(n, rp, col, val, x_host, budget_s=10.0, max_reps=200)
+        cpu = {"value": round(2.0 * nnz_loc / t / 1e9, 3), "unit": "GFlop/s", "cores": cores, "kind": "oracle",
+               "sample": f"whole {a.config} matrix ({nnz_loc} nnz), {reps} products, median; {tot:.1f} s of "
+                         f"oracle_spmv_crs ({np.dtype(npdt).name}, OpenMP {cores} threads)"}
     nnz = nnz_loc
     if world > 1:
-        t = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
-        dist.all_reduce(t)
-        nnz = int(t.item())
-    x = torch.from_numpy(inputs.vector(hi - lo, npdt, i0=lo)).to(dev)
+        tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
+        dist.all_reduce(tt)
+        nnz = int(tt.item())
+    x = torch.from_numpy(x_host).to(dev)
     y = torch.empty(hi - lo, dtype=tdt, device=dev)
+    if permuted:
+        xp = torch.empty_like(x)
+        A.to_permuted(xp, x)  # once, before the "iterative scheme"
+        x = xp
     t_setup = time.perf_counter() - t_setup
 
-    # roofline denominator measured in this run (copy and read streams; max taken)
+    # roofline denominator measured in this run (copy and read streams)
     probe_copy, probe_read = pj.bw_probe(a.probe_bytes, 5)
-    peaks = measured_peaks()
-    peak_file = peaks.get("hbm_gbs")
-
+    peak_file = measured_peaks().get("hbm_gbs")
     stream = torch.cuda.current_stream()
 
     def step():
@@ -221,30 +229,33 @@ def main():
         else:
             A.spmv(y, x, stream=stream)
 
+    def timed(fn, k):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / k
+
     for _ in range(max(a.warmup, 3)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     launches0 = pj.launch_count()
     with ClockSampler(local_rank) as clk:
-        e0.record(stream)
-        for _ in range(a.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
+        ms = timed(step, a.steps)
     launches = pj.launch_count() - launches0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.steps
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
         dist.all_reduce(lt)
         launches = int(lt.item())
@@ -255,35 +266,49 @@ def main():
     achieved = b_min / t_s / 1e9 / world  # per GPU
     peak = peak_file if peak_file else max(probe_copy, probe_read)
 
-    # end-to-end through the public API with host buffers (H2D x, kernel, D2H y per step)
+    # side-by-side kernels on the same matrix (N=1): rows-only pJDS and ELLPACK-R
+    if world == 1 and a.impl == "pjds" and not a.no_compare:
+        x0 = torch.from_numpy(x_host).to(dev)
+        for name, mk in (("pjds_rows_only" if permuted else "pjds_permuted",
+                          lambda: pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows,
+                                                         symmetric=not permuted)),
+                         ("ellpack_r", lambda: pj.EllrMatrix.from_crs(n, rp, col, val))):
+            B = mk()
+            for _ in range(3):
+                B.spmv(y, x0, stream=stream)
+            mb = timed(lambda: B.spmv(y, x0, stream=stream), 20)
+            compare[name] = {"GFlop/s": round(2.0 * nnz / (mb * 1e-3) / 1e9, 1), "ms": round(mb, 4),
+                             "frac": round(b_min / (mb * 1e-3) / 1e9 / peak, 4),
+                             "bytes": B.info["bytes_total"]}
+            del B
+            torch.cuda.synchronize()
+        del x0
+    del col, val
+
+    # end-to-end through the public API with host buffers in the original basis (H2D x, basis
+    # change, kernel, basis change back, D2H y, every step)
     e2e = None
     if world == 1 and a.impl == "pjds":
-        xh = torch.from_numpy(inputs.vector(n, npdt)).pin_memory().numpy()
+        xh = torch.from_numpy(x_host).pin_memory().numpy()
         yh = torch.empty(n, dtype=tdt).pin_memory().numpy()
         A.spmv_host(yh, xh)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(a.e2e_steps):
-            A.spmv_host(yh, xh)
-        te = (time.perf_counter() - t0) / a.e2e_steps
-        e2e = {"value": 2.0 * nnz / te / 1e9, "unit": "GFlop/s", "h2d_bytes_per_step": n * sv,
-               "d2h_bytes_per_step": n * sv, "ms_per_step": te * 1e3}
+        te = timed(lambda: A.spmv_host(yh, xh), a.e2e_steps) * 1e-3
+        e2e = {"value": round(2.0 * nnz / te / 1e9, 2), "unit": "GFlop/s", "h2d_bytes_per_step": n * sv,
+               "d2h_bytes_per_step": n * sv, "ms_per_step": round(te * 1e3, 3)}
     elif world > 1:
-        e2e = {"value": None, "unit": "GFlop/s", "note": "host-buffer e2e is measured at N=1 only",
+        e2e = {"value": None, "unit": "GFlop/s", "note": "host-buffer e2e is measured at N=1",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
-
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(a.config, npdt)
 
     if rank == 0:
         wl = f"{a.config}: {CONFIG_DESC[a.config]}, nnz={nnz}, {a.dtype}, {a.impl}"
+        if world == 1 and a.impl == "pjds":
+            wl += ", permuted basis (PAPER.md L241-246)" if permuted else ", original basis (rows permuted)"
         out = {
             "metric": METRIC,
             "value": round(gflops, 2), "unit": "GFlop/s", "n_gpus": world, "steps": a.steps,
             "warmup": max(a.warmup, 3), "ms_per_step": round(ms, 5), "higher_is_better": True,
-            "scaling": "strong",
-            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
+            "scaling": "strong", "vs_baseline": None, "dtype": a.dtype,
+            "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
             "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows,
                        "parallelism": f"row-partition r{world}" if world > 1 else "single GPU",
                        "overlap": (not a.no_overlap) if world > 1 else None,
@@ -300,6 +325,7 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "footprint": footprint,
+            "compare": compare or None,
             "setup_s": round(t_setup, 2),
         }
         print(json.dumps(out), flush=True)
@@ -312,33 +338,21 @@ def main():
 
 def reference_arm(a, world, npdt):
     """--impl reference: the oracle (plain CRS, OpenMP over all host cores) on the same config,
-    metric and unit; each step is a bounded sample of the workload (a leading row block)."""
+    metric and unit; each step is one product over the whole matrix, bounded to ~2 minutes."""
     import inputs
-    import oracle
     g = inputs.Generator.from_config(a.config)
-    rows = min(g.n, 4_000_000)
-    rp, col, val = g.crs(0, rows, dtype=npdt)
+    rp, col, val = g.crs(dtype=npdt)
     x = inputs.vector(g.n, npdt)
-    cores = len(os.sched_getaffinity(0))
     nnz = int(rp[-1])
-    for _ in range(max(a.warmup, 1)):
-        oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)
-    steps = a.steps
-    t0 = time.perf_counter()
-    deadline = t0 + 120.0
-    done = 0
-    while done < steps and time.perf_counter() < deadline:
-        oracle.spmv_crs(rows, rp, col, val, x, nthreads=cores)
-        done += 1
-    t = (time.perf_counter() - t0) / done
+    t, reps, cores, tot = time_oracle(g.n, rp, col, val, x, budget_s=120.0, max_reps=a.steps)
     v = 2.0 * nnz / t / 1e9
-    sample = f"rows [0,{rows}) of {a.config} ({nnz} nnz) per step, {done} steps"
+    sample = f"whole {a.config} matrix ({nnz} nnz) per step, {reps} steps (median), oracle_spmv_crs"
     print(json.dumps({
         "impl": "reference", "metric": METRIC,
-        "value": round(v, 3), "unit": "GFlop/s", "n_gpus": world, "steps": done, "warmup": max(a.warmup, 1),
+        "value": round(v, 3), "unit": "GFlop/s", "n_gpus": world, "steps": reps, "warmup": 1,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": a.dtype, "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
-        "config": {"workload": f"{a.config}: {CONFIG_DESC[a.config]}, CPU oracle CRS (sample)"},
+        "config": {"workload": f"{a.config}: {CONFIG_DESC[a.config]}, nnz={nnz}, CPU oracle CRS"},
         "cpu_baseline": {"value": round(v, 3), "unit": "GFlop/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)

@@ -87,8 +87,17 @@ int pjds_destroy(pjds_t A);
 int pjds_spmv(pjds_t A, void* y, const void* x, void* stream);
 
 /*
- * pjds_spmv_host — end-to-end variant with HOST x / y (any host memory; pinned is faster):
- * copies x host->device, runs pjds_spmv, copies y device->host, and synchronises `stream`.
+ * pjds_permute — basis change for the permuted-basis mode ("permutation of
+ * the indices needs to be done only before the start and after the end of the algorithm"):
+ * direction 0: dst[k] = src[perm[k]] (original -> permuted), 1: dst[perm[k]] = src[k] (back).
+ * Device pointers of n entries, handle dtype; dst must not alias src.  Any handle may be used.
+ */
+int pjds_permute(pjds_t A, void* dst, const void* src, int32_t direction, void* stream);
+
+/*
+ * pjds_spmv_host — end-to-end variant with HOST x / y in the ORIGINAL basis (any host memory;
+ * pinned is faster): copies x host->device, (PJDS_PERM_SYMMETRIC: permutes x to the permuted
+ * basis), runs the pJDS kernel, (permutes y back), copies y device->host, synchronises `stream`.
  * The transfer cost is the paper's T_PCI (Eq. 2).  Staging buffers are
  * allocated on first use and owned by the handle.
  */
@@ -221,6 +230,13 @@ int pjds_nccl_unique_id(void* out128);
    `bytes` of device memory `reps` times; returns best GB/s of a copy (read+write bytes) and of a
    read-only reduction.  Allocates and frees its own buffers. */
 int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs);
+
+/* Tuning knob (process-wide): pJDS kernel variant with `rows_per_thread` R in {1,2,4} consecutive
+   sorted rows per thread (vector loads, R independent FMA chains) and j-unroll `unroll` in {2,4,8}.
+   (0, 0) restores the automatic choice.  R is reduced until it divides block_rows.  Every
+   variant computes bit-identical y (one FMA chain per row, stored order).  unroll + 16 also
+   enables a tile-wide L2 bulk prefetch of val/col (measured slower; kept for A/B runs). */
+int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
 
 /* Number of kernel launches this library has enqueued (process-wide counter). */
 int64_t pjds_launch_count(void);

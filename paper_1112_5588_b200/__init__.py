@@ -100,8 +100,21 @@ class PjdsMatrix:
              _stream_ptr(stream))
         return y
 
+    def to_permuted(self, dst, src, stream=None):
+        """dst[k] = src[perm[k]] on the GPU (basis change before an iterative scheme)."""
+        call("pjds_permute", self._h, _check_vec(dst, self.n, self.dtype, "dst"), _check_vec(src, self.n, self.dtype, "src"),
+             0, _stream_ptr(stream))
+        return dst
+
+    def from_permuted(self, dst, src, stream=None):
+        """dst[perm[k]] = src[k] on the GPU (basis change after the iterative scheme)."""
+        call("pjds_permute", self._h, _check_vec(dst, self.n, self.dtype, "dst"), _check_vec(src, self.n, self.dtype, "src"),
+             1, _stream_ptr(stream))
+        return dst
+
     def spmv_host(self, y, x, stream=None):
-        """End-to-end y = A x with host numpy arrays (H2D x, kernel, D2H y, synchronised)."""
+        """End-to-end y = A x with host numpy arrays in the ORIGINAL basis (H2D x, [permute], kernel,
+        [permute back], D2H y, synchronised)."""
         nd = _np_dtype(self.dtype)
         assert x.dtype == nd and y.dtype == nd and x.flags.c_contiguous and y.flags.c_contiguous
         assert len(x) >= self.n and len(y) >= self.n

@@ -55,6 +55,7 @@ _SIGS = {
     "pjds_destroy": [c_p],
     "pjds_spmv": [c_p, c_p, c_p, c_p],
     "pjds_spmv_host": [c_p, c_p, c_p, c_p],
+    "pjds_permute": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_info": [c_p, c_p],
     "pjds_histogram": [c_p, c_p, c_i32],
     "pjds_export": [c_p, c_p, c_p, c_p, c_p, c_p],
@@ -76,6 +77,7 @@ _SIGS = {
     "pjds_nccl_load": [ctypes.c_char_p],
     "pjds_nccl_unique_id": [c_p],
     "pjds_bw_probe": [c_i64, c_i32, c_p, c_p],
+    "pjds_set_kernel_variant": [c_i32, c_i32],
 }
 EXPORTED = sorted(list(_SIGS) + ["pjds_launch_count", "pjds_last_error", "pjds_version"])
 

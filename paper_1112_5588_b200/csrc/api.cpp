@@ -78,10 +78,9 @@ int pjds_create_from_crs(pjds_t* out, int64_t n, const int64_t* rowptr, const in
   int s = convert_pjds(A->h, n, n, rowptr, col, val, dtype, block_rows, flags & PJDS_PERM_SYMMETRIC);
   if (s == PJDS_OK && !(flags & PJDS_HOST_ONLY)) {
     if (flags & PJDS_PERM_SYMMETRIC) {
-      // permuted basis: y_perm[k] is stored at k (identity store map)
-      std::vector<int32_t> ident(n);
-      for (int64_t k = 0; k < n; ++k) ident[A->h.perm[k]] = (int32_t)k;  // perm[k] -> k
-      s = upload_pjds(A, ident.data());
+      // permuted basis: y_perm[k] is stored at k; the kernel does not read perm at all
+      A->direct_store = true;
+      s = upload_pjds(A, nullptr);
     } else {
       s = upload_pjds(A, nullptr);
     }
@@ -119,16 +118,34 @@ int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream) {
   if (!A || !y_host || !x_host) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host: NULL argument");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host: handle is host-only");
   const size_t bytes_x = (size_t)A->ncols * dtype_size(A->h.dtype), bytes_y = (size_t)A->h.n * dtype_size(A->h.dtype);
+  const bool sym = A->direct_store;
   if (!A->d_xs) {
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_xs, bytes_x ? bytes_x : 16));
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_ys, bytes_y ? bytes_y : 16));
+    // symmetric: two extra vectors for the basis change before / after the product
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_xs, (bytes_x ? bytes_x : 16) * (sym ? 2 : 1)));
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_ys, (bytes_y ? bytes_y : 16) * (sym ? 2 : 1)));
   }
   cudaStream_t s = (cudaStream_t)stream;
   PJDS_CUDA_TRY(cudaMemcpyAsync(A->d_xs, x_host, bytes_x, cudaMemcpyHostToDevice, s));
-  PJDS_TRY(launch_pjds_spmv(A, A->d_ys, A->d_xs, s, false));
+  if (sym) {  // host vectors are in the ORIGINAL basis: permute once before and once after
+    char* xp = (char*)A->d_xs + (bytes_x ? bytes_x : 16);
+    char* yp = (char*)A->d_ys + (bytes_y ? bytes_y : 16);
+    PJDS_TRY(launch_permute(A->d_perm, A->h.n, A->d_xs, xp, A->h.dtype, 0, s));
+    PJDS_TRY(launch_pjds_spmv(A, yp, xp, s, false));
+    PJDS_TRY(launch_permute(A->d_perm, A->h.n, yp, A->d_ys, A->h.dtype, 1, s));
+  } else {
+    PJDS_TRY(launch_pjds_spmv(A, A->d_ys, A->d_xs, s, false));
+  }
   PJDS_CUDA_TRY(cudaMemcpyAsync(y_host, A->d_ys, bytes_y, cudaMemcpyDeviceToHost, s));
   PJDS_CUDA_TRY(cudaStreamSynchronize(s));
   return PJDS_OK;
+}
+
+int pjds_permute(pjds_t A, void* dst, const void* src, int32_t direction, void* stream) {
+  if (!A || (A->h.n > 0 && (!dst || !src))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: NULL argument");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: handle is host-only");
+  if (dst == src) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: dst aliases src");
+  if (direction != 0 && direction != 1) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: direction 0 or 1");
+  return launch_permute(A->d_perm, A->h.n, src, dst, A->h.dtype, direction, (cudaStream_t)stream);
 }
 
 int pjds_info(pjds_t A, pjds_info_t* o) {
@@ -251,6 +268,10 @@ int ellr_export(ellr_t A, int32_t* rowmax, int32_t* col, void* val) {
     if (val) std::memcpy(val, h.val.data(), vb);
   }
   return PJDS_OK;
+}
+
+int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll) {
+  return set_kernel_variant(rows_per_thread, unroll);
 }
 
 int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs) {

@@ -70,6 +70,7 @@ struct pjds_mat {
   void* d_xs = nullptr;       // staging for pjds_spmv_host
   void* d_ys = nullptr;
   int64_t ncols = 0;
+  bool direct_store = false;  // permuted basis: y[k] stored contiguously, perm not read
 };
 
 struct ellr_mat {
@@ -89,7 +90,9 @@ int free_pjds_device(pjds_mat* A);
 // ---- kernel launchers (kernels.cu) -----------------------------------------------------------
 int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool accumulate);
 int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s);
+int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, int dtype, int back, cudaStream_t s);
 int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int dtype, cudaStream_t s);
+int set_kernel_variant(int r, int u);
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
 void count_launch(int64_t k = 1);
 }  // namespace pjds

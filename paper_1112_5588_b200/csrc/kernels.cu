@@ -85,57 +85,106 @@ __device__ __forceinline__ float ld_rhs(const float* p, uint64_t pol) {
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
-// R-wide vector of T / int for the rows a thread owns
-template <typename T, int R> struct VecT;
-template <typename T> struct VecT<T, 1> {
+// R-wide vector of T / int for the R consecutive sorted rows a thread owns (one jagged column)
+template <typename T, int R> struct Vec;
+template <typename T> struct Vec<T, 1> {
   T v[1];
   __device__ __forceinline__ void load(const T* p, uint64_t pol) { v[0] = ld_stream(p, pol); }
 };
-template <typename T> struct VecT<T, 2> {
+template <typename T> struct Vec<T, 2> {
   T v[2];
   __device__ __forceinline__ void load(const T* p, uint64_t pol) {
     auto t = ld_stream2(p, pol);
     v[0] = t.x; v[1] = t.y;
   }
 };
+template <> struct Vec<double, 4> {  // 256-bit LDG (sm_100): L2 evict-first is encoded in the op
+  double v[4];
+  __device__ __forceinline__ void load(const double* p, uint64_t) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  }
+};
+template <> struct Vec<float, 4> {
+  float v[4];
+  __device__ __forceinline__ void load(const float* p, uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
+  }
+};
+template <> struct Vec<int, 4> {
+  int v[4];
+  __device__ __forceinline__ void load(const int* p, uint64_t pol) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(p), "l"(pol));
+  }
+};
 
 constexpr int kThreads = 256;
 constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
 
+// Store modes: y[perm[k]] = acc (row-only basis), y[k] = acc (permuted basis, PJDS_PERM_SYMMETRIC),
+// y[perm[k]] += acc (dist nonlocal part: the result is written twice).
+enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2 };
+
 // ---- pJDS kernel -----------------------------------------------------------------------------
-// Thread t of the grid owns sorted rows k = R*t .. R*t+R-1 (consecutive, same pJDS block since
-// b_r is a multiple of 32*R... the launcher guarantees b_r % (32*R) == 0).  Rows of a warp lie in
-// one block, so the loop bound block_len[b] is warp-uniform (reading 6).
-template <typename T, typename Off, int R, int U, bool ACC>
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+// Thread t owns the R consecutive sorted rows k0 = R*t .. R*t+R-1 (R divides b_r, so they share
+// one pJDS block and its length).  A warp covers 32R rows = one or several consecutive blocks;
+// lanes of a block loop to that block's length (PAPER.md L219-222 / Listing 2, reading 6).
+// PF: before computing, lane 0 of each warp issues one L2 bulk prefetch (UBLKPF) per jagged
+// column for the warp's contiguous val/col segment, so the HBM stream of the whole warp tile is
+// in flight at once, independent of registers; the loads below then hit L2.
+// Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
+template <typename T, typename Off, int R, int U, int MODE, bool PF>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br) {
   __shared__ Off s_cs[kSmemCS];
-  const int64_t k0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * R;  // first row of this thread
+  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  const int64_t k0 = t * R;
   const int64_t cta_k0 = (int64_t)blockIdx.x * kThreads * R;
-  // longest block of the CTA is its first one (sorted descending)
-  const int cta_len = block_len[cta_k0 / br];
+  const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
   const int lim = min(cta_len + 1, kSmemCS);
   for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
   __syncthreads();
   if (k0 >= n_pad) return;
-  const int len = block_len[k0 / br];
+  const int64_t warp_k0 = (t & ~int64_t(31)) * R;
+  const int wlen = block_len[warp_k0 / br];
+  const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
+  auto cs = [&](int j) -> Off { return j < kSmemCS ? s_cs[j] : (Off)col_start[j]; };
+  if (PF) {
+    if ((threadIdx.x & 31) == 0) {
+      for (int j = 0; j < wlen; ++j) {
+        const Off o = cs(j) + (Off)warp_k0;
+        const Off e = min(o + (Off)(32 * R), cs(j + 1));  // stay inside jagged column j
+        if (e > o) {
+          prefetch_l2(val + o, (uint32_t)((e - o) * sizeof(T)), pol_s);
+          prefetch_l2(col + o, (uint32_t)((e - o) * 4), pol_s);
+        }
+      }
+    }
+    __syncwarp();
+  }
   T acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = T(0);
-  auto cs = [&](int j) -> Off { return j < kSmemCS ? s_cs[j] : (Off)col_start[j]; };
   int j = 0;
-  for (; j + U <= len; j += U) {
-    VecT<T, R> v[U];
-    VecT<int, R> c[U];
+  for (; j + U <= len; j += U) {  // full chunks: no predicates, all U loads issued back to back
+    Vec<T, R> v[U];
+    Vec<int, R> c[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const Off off = cs(j + u) + (Off)k0;
-      v[u].load(val + off, pol_s);
-      c[u].load(col + off, pol_s);
+      const Off o = cs(j + u) + (Off)k0;
+      v[u].load(val + o, pol_s);
+      c[u].load(col + o, pol_s);
     }
     T xv[U][R];
 #pragma unroll
@@ -148,16 +197,15 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
       for (int r = 0; r < R; ++r) acc[r] = fma_rn(v[u].v[r], xv[u][r], acc[r]);
   }
   if (j < len) {  // ragged tail of the j-loop: predicated, same chain order
-    VecT<T, R> v[U];
-    VecT<int, R> c[U];
+    Vec<T, R> v[U];
+    Vec<int, R> c[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < U; ++u)
       if (j + u < len) {
-        const Off off = cs(j + u) + (Off)k0;
-        v[u].load(val + off, pol_s);
-        c[u].load(col + off, pol_s);
+        const Off o = cs(j + u) + (Off)k0;
+        v[u].load(val + o, pol_s);
+        c[u].load(col + o, pol_s);
       }
-    }
     T xv[U][R];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -174,74 +222,130 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   for (int r = 0; r < R; ++r) {
     const int64_t k = k0 + r;
     if (k < n) {
-      const int p = perm[k];
-      if (ACC) y[p] = y[p] + acc[r];
-      else y[p] = acc[r];
+      if (MODE == STORE_DIRECT) {
+        y[k] = acc[r];
+      } else {
+        const int p = perm[k];
+        if (MODE == STORE_PERM_ACC) y[p] = y[p] + acc[r];
+        else y[p] = acc[r];
+      }
     }
   }
 }
 
+static bool g_prefetch = false;  // measured: the tile-wide L2 bulk prefetch slows every config
+
 template <typename T, typename Off, int R, int U>
-int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, bool accumulate) {
+int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode) {
   const auto& h = A->h;
   const int64_t threads = h.n_pad / R;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
-  if (accumulate)
-    pjds_spmv_kernel<T, Off, R, U, true><<<(unsigned)grid, kThreads, 0, s>>>(
-        (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br);
-  else
-    pjds_spmv_kernel<T, Off, R, U, false><<<(unsigned)grid, kThreads, 0, s>>>(
-        (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br);
+#define PJDS_LAUNCH_PF(M, PF)                                                                            \
+  pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br)
+#define PJDS_LAUNCH(M)             \
+  if (g_prefetch) PJDS_LAUNCH_PF(M, true); \
+  else PJDS_LAUNCH_PF(M, false)
+  if (mode == STORE_DIRECT) {
+    PJDS_LAUNCH(STORE_DIRECT);
+  } else if (mode == STORE_PERM_ACC) {
+    PJDS_LAUNCH(STORE_PERM_ACC);
+  } else {
+    PJDS_LAUNCH(STORE_PERM);
+  }
+#undef PJDS_LAUNCH
+#undef PJDS_LAUNCH_PF
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;
 }
 
-template <typename T>
-int launch_pjds_dt(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool acc) {
-  const bool off32 = A->h.stored + A->h.n_pad < (int64_t(1) << 31);
-  const bool r2 = A->h.br % 64 == 0;
-  if (off32) {
-    if (r2) return launch_pjds_t<T, int32_t, 2, 4>(A, (T*)y, (const T*)x, s, acc);
-    return launch_pjds_t<T, int32_t, 1, 8>(A, (T*)y, (const T*)x, s, acc);
+// kernel variant (rows per thread R, j-unroll U); 0 = automatic choice
+static int g_var_r = 0, g_var_u = 0;
+
+template <typename T, typename Off>
+int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode) {
+  int R = g_var_r, U = g_var_u;
+  if (R == 0) {
+    // enough warps to cover the SMs several times: R = 4 (256-bit DP loads) for large matrices,
+    // R = 2 / 1 when n_pad / R would leave the GPU short of warps (long-row matrices like DLR1)
+    const int64_t np = A->h.n_pad;
+    if (np / 4 >= (int64_t(1) << 19)) { R = 4; U = 2; }
+    else if (np / 2 >= (int64_t(1) << 17)) { R = 2; U = 4; }
+    else { R = 1; U = 8; }
   }
-  if (r2) return launch_pjds_t<T, int64_t, 2, 4>(A, (T*)y, (const T*)x, s, acc);
-  return launch_pjds_t<T, int64_t, 1, 8>(A, (T*)y, (const T*)x, s, acc);
+  while (A->h.br % R) R >>= 1;  // R must divide b_r
+  T* yy = (T*)y;
+  const T* xx = (const T*)x;
+  if (R == 4) return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode) : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode);
+  if (R == 2) return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode) : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode);
+  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode);
+}
+
+template <typename T>
+int launch_pjds_dt(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode) {
+  const bool off32 = A->h.stored + A->h.n_pad < (int64_t(1) << 31);
+  if (off32) return launch_pjds_off<T, int32_t>(A, y, x, s, mode);
+  return launch_pjds_off<T, int64_t>(A, y, x, s, mode);
 }
 
 // ---- ELLPACK-R kernel ------------------------------------------------------------------------
-// One thread per row, consecutive rows to consecutive threads; the loop runs
-// to the warp's longest row with per-lane predication j < rowmax[i] (L187-191).
-template <typename T, int U>
+// Consecutive rows to consecutive threads, R consecutive rows per thread with
+// vector loads of val[j*N_pad + i .. +R-1]; each row stops at its own rowmax[i] ("threads only
+// execute non-zero contributions", L187-191) while the warp runs to its longest row.
+template <typename T, int R, int U>
 __global__ void __launch_bounds__(kThreads)
 ellr_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int* __restrict__ rowmax,
                  const T* __restrict__ x, T* __restrict__ y, int64_t n, int64_t n_pad) {
-  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  if (i >= n_pad) return;
-  const int len = rowmax[i];
-  const int wlen = __reduce_max_sync(0xffffffffu, len);
+  const int64_t i0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * R;
+  if (i0 >= n_pad) return;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
-  T acc = T(0);
-  for (int j = 0; j < wlen; j += U) {
-    T v[U];
-    int c[U];
+  Vec<int, R> lens;
+  lens.load(rowmax + i0, pol_s);
+  int tmax = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) tmax = max(tmax, lens.v[r]);
+  const int wmax = __reduce_max_sync(__activemask(), tmax);
+  T acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = T(0);
+  for (int j = 0; j < wmax; j += U) {
+    Vec<T, R> v[U];
+    Vec<int, R> c[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j + u < len) {
-        v[u] = ld_stream(val + (int64_t)(j + u) * n_pad + i, pol_s);
-        c[u] = ld_stream(col + (int64_t)(j + u) * n_pad + i, pol_s);
+      if (j + u < tmax) {
+        const int64_t off = (int64_t)(j + u) * n_pad + i0;
+        v[u].load(val + off, pol_s);
+        c[u].load(col + off, pol_s);
       }
-    T xv[U];
+    T xv[U][R];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j + u < len) xv[u] = ld_rhs(x + c[u], pol_x);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (j + u < lens.v[r]) xv[u][r] = ld_rhs(x + c[u].v[r], pol_x);
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j + u < len) acc = fma_rn(v[u], xv[u], acc);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (j + u < lens.v[r]) acc[r] = fma_rn(v[u].v[r], xv[u][r], acc[r]);
   }
-  if (i < n) y[i] = acc;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (i0 + r < n) y[i0 + r] = acc[r];
+}
+
+// basis change: to permuted dst[k] = src[perm[k]]; back dst[perm[k]] = src[k]
+template <typename T>
+__global__ void permute_kernel(const int* __restrict__ perm, int64_t n, const T* __restrict__ src, T* __restrict__ dst,
+                               int back) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    if (back) dst[perm[k]] = src[k];
+    else dst[k] = src[perm[k]];
+  }
 }
 
 template <typename T>
@@ -267,20 +371,46 @@ __global__ void read_kernel(const int4* __restrict__ a, int64_t n, int* __restri
 }  // namespace
 
 int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool accumulate) {
-  if (A->h.dtype == PJDS_F64) return launch_pjds_dt<double>(A, y, x, s, accumulate);
-  return launch_pjds_dt<float>(A, y, x, s, accumulate);
+  const int mode = accumulate ? STORE_PERM_ACC : (A->direct_store ? STORE_DIRECT : STORE_PERM);
+  if (A->h.dtype == PJDS_F64) return launch_pjds_dt<double>(A, y, x, s, mode);
+  return launch_pjds_dt<float>(A, y, x, s, mode);
+}
+
+int set_kernel_variant(int r, int u) {
+  // u >= 16 encodes "with the tile-wide L2 bulk prefetch" (u - 16) for A/B measurements
+  const bool pf = u >= 16;
+  if (u >= 16) u -= 16;
+  if (!((r == 0 && u == 0) || ((r == 1 || r == 2 || r == 4) && (u == 2 || u == 4 || u == 8))))
+    return set_error(PJDS_ERR_INVALID_ARG, "variant: rows_per_thread in {1,2,4}, unroll in {2,4,8} (or 0,0)");
+  g_var_r = r;
+  g_var_u = u;
+  g_prefetch = pf;
+  return PJDS_OK;
 }
 
 int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
   const auto& h = A->h;
-  const int64_t grid = (h.n_pad + kThreads - 1) / kThreads;
+  constexpr int R = 2, U = 4;
+  const int64_t grid = (h.n_pad / R + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
   if (h.dtype == PJDS_F64)
-    ellr_spmv_kernel<double, 8><<<(unsigned)grid, kThreads, 0, s>>>((const double*)A->d_val, A->d_col, A->d_rowmax,
-                                                                    (const double*)x, (double*)y, h.n, h.n_pad);
+    ellr_spmv_kernel<double, R, U><<<(unsigned)grid, kThreads, 0, s>>>((const double*)A->d_val, A->d_col, A->d_rowmax,
+                                                                       (const double*)x, (double*)y, h.n, h.n_pad);
   else
-    ellr_spmv_kernel<float, 8><<<(unsigned)grid, kThreads, 0, s>>>((const float*)A->d_val, A->d_col, A->d_rowmax,
-                                                                  (const float*)x, (float*)y, h.n, h.n_pad);
+    ellr_spmv_kernel<float, R, U><<<(unsigned)grid, kThreads, 0, s>>>((const float*)A->d_val, A->d_col, A->d_rowmax,
+                                                                     (const float*)x, (float*)y, h.n, h.n_pad);
+  count_launch();
+  PJDS_CUDA_TRY(cudaGetLastError());
+  return PJDS_OK;
+}
+
+int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, int dtype, int back, cudaStream_t s) {
+  if (n <= 0) return PJDS_OK;
+  const int64_t grid = std::min<int64_t>((n + 255) / 256, 148 * 32);
+  if (dtype == PJDS_F64)
+    permute_kernel<double><<<(unsigned)grid, 256, 0, s>>>(perm, n, (const double*)src, (double*)dst, back);
+  else
+    permute_kernel<float><<<(unsigned)grid, 256, 0, s>>>(perm, n, (const float*)src, (float*)dst, back);
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;

@@ -220,3 +220,47 @@ def test_misuse_errors(pj):
         A.spmv(x, x)  # aliasing
     with pytest.raises(ValueError):
         A.spmv(torch.empty(n, dtype=torch.float32, device="cuda"), x)
+
+
+@pytest.mark.parametrize("variant", [(1, 8), (2, 4), (2, 8), (4, 2), (4, 4)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_kernel_variants_bitwise(pj, variant, dtype):
+    """Every (rows per thread, unroll) variant gives the same per-row FMA chain."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_kernel_variant(*variant) == 0
+        for kind, n, br in (("random", 3001, 32), ("empty_rows", 999, 64), ("clustered", 4100, 128)):
+            _, rp, col, val = inputs.small(kind, n, seed=5, dtype=dtype)
+            x = inputs.vector(n, dtype)
+            for sym in (False, True):
+                A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, symmetric=sym)
+                y = torch.full((n,), float("nan"), dtype=torch.float64 if dtype == np.float64 else torch.float32,
+                               device="cuda")
+                perm = A.export()["perm"]
+                A.spmv(y, tdev(x[perm] if sym else x))
+                yh = y.cpu().numpy()
+                if sym:
+                    yo = np.empty(n, dtype=yh.dtype)
+                    yo[perm] = yh
+                    yh = yo
+                check_y(yh, n, rp, col, val, x)
+    finally:
+        L.pjds_set_kernel_variant(0, 0)
+
+
+def test_permute_and_symmetric_host_e2e(pj):
+    """Basis change kernels and the e2e host path of the permuted-basis mode."""
+    n, rp, col, val = inputs.config_crs("C1")
+    x = inputs.vector(n)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+    perm = A.export()["perm"]
+    xt = tdev(x)
+    xp = torch.empty_like(xt)
+    A.to_permuted(xp, xt)
+    assert np.array_equal(xp.cpu().numpy(), x[perm])
+    back = torch.empty_like(xt)
+    A.from_permuted(back, xp)
+    assert np.array_equal(back.cpu().numpy(), x)
+    y = np.empty(n)
+    A.spmv_host(y, x)
+    check_y(y, n, rp, col, val, x)

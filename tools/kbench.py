@@ -1,0 +1,52 @@
+"""Kernel sweep (development tool): every config x format x dtype, CUDA-event timed, one JSON line each.
+Not the bench contract (bench.py is); used to pick kernel variants and to drive ncu passes."""
+import argparse, json, os, sys, time
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import inputs
+import paper_1112_5588_b200 as pj
+
+p = argparse.ArgumentParser()
+p.add_argument("--configs", default="C2,C3,C4,C5")
+p.add_argument("--dtypes", default="f64,f32")
+p.add_argument("--fmts", default="pjds32,pjds64,pjds128,ellr")
+p.add_argument("--reps", type=int, default=30)
+p.add_argument("--variants", default="0x0")
+p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
+a = p.parse_args()
+peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
+for cfg in a.configs.split(","):
+    for dts in a.dtypes.split(","):
+        npdt = np.float64 if dts == "f64" else np.float32
+        sv = np.dtype(npdt).itemsize
+        n, rp, col, val = inputs.config_crs(cfg, dtype=npdt)
+        nnz = len(col)
+        x = torch.from_numpy(inputs.vector(n, npdt)).cuda()
+        y = torch.empty_like(x)
+        bmin = nnz * (sv + 4) + 2 * n * sv
+        for fmt in a.fmts.split(","):
+          if fmt.startswith("pjds"):
+              sym = fmt.endswith("s")
+              A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=int(fmt[4:].rstrip("s")), symmetric=sym)
+          else:
+              A = pj.EllrMatrix.from_crs(n, rp, col, val)
+          for var in a.variants.split(","):
+            vr, vu = map(int, var.split("x"))
+            pj.lib().pjds_set_kernel_variant(vr, vu)
+            if fmt == "ellr" and var != a.variants.split(",")[0]: continue
+            if a.once:
+                A.spmv(y, x); torch.cuda.synchronize(); continue
+            for _ in range(5): A.spmv(y, x)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps): A.spmv(y, x)
+            e1.record(); torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / a.reps * 1e-3
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+                              "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
+                              "stored_bytes": A.info.get("bytes_total")}), flush=True)
+          del A
+        del rp, col, val
