@@ -238,6 +238,11 @@ int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gb
    enables a tile-wide L2 bulk prefetch of val/col (measured slower; kept for A/B runs). */
 int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
 
+/* Tuning knob (process-wide): L2 eviction priority of the pJDS kernel's streamed val/col loads
+   and of its x gathers; kinds 0 evict_normal, 1 evict_first, 2 evict_last, 3 evict_unchanged.
+   Default (1, 2).  Results are unaffected. */
+int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind);
+
 /* Number of kernel launches this library has enqueued (process-wide counter). */
 int64_t pjds_launch_count(void);
 

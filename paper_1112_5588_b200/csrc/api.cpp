@@ -274,6 +274,8 @@ int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll) {
   return set_kernel_variant(rows_per_thread, unroll);
 }
 
+int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind) { return set_cache_policy(stream_kind, x_kind); }
+
 int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs) {
   if (!copy_gbs || !read_gbs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_bw_probe: NULL argument");
   return bw_probe(bytes, reps, copy_gbs, read_gbs);

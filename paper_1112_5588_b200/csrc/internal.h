@@ -93,6 +93,7 @@ int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s);
 int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, int dtype, int back, cudaStream_t s);
 int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int dtype, cudaStream_t s);
 int set_kernel_variant(int r, int u);
+int set_cache_policy(int stream_kind, int x_kind);
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
 void count_launch(int64_t k = 1);
 }  // namespace pjds

@@ -37,6 +37,15 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// L2 eviction policy by kind: 0 evict_normal, 1 evict_first, 2 evict_last, 3 evict_unchanged
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+  uint64_t p;
+  if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 3) asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 // streaming (read once): no L1 allocation, L2 evict-first
 __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
   double v;
@@ -144,7 +153,7 @@ template <typename T, typename Off, int R, int U, int MODE, bool PF>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
-                 T* __restrict__ y, int64_t n, int64_t n_pad, int br) {
+                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol) {
   __shared__ Off s_cs[kSmemCS];
   const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   const int64_t k0 = t * R;
@@ -157,8 +166,8 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const int64_t warp_k0 = (t & ~int64_t(31)) * R;
   const int wlen = block_len[warp_k0 / br];
   const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
-  const uint64_t pol_s = policy_evict_first();
-  const uint64_t pol_x = policy_evict_last();
+  const uint64_t pol_s = make_policy(pol & 0xff);
+  const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
   auto cs = [&](int j) -> Off { return j < kSmemCS ? s_cs[j] : (Off)col_start[j]; };
   if (PF) {
     if ((threadIdx.x & 31) == 0) {
@@ -233,6 +242,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   }
 }
 
+static int g_pol = 1 | (2 << 8);  // val/col evict_first, x evict_last
 static bool g_prefetch = false;  // measured: the tile-wide L2 bulk prefetch slows every config
 
 template <typename T, typename Off, int R, int U>
@@ -243,7 +253,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode)
   if (grid == 0) return PJDS_OK;
 #define PJDS_LAUNCH_PF(M, PF)                                                                            \
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
-      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br)
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol)
 #define PJDS_LAUNCH(M)             \
   if (g_prefetch) PJDS_LAUNCH_PF(M, true); \
   else PJDS_LAUNCH_PF(M, false)
@@ -374,6 +384,13 @@ int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, 
   const int mode = accumulate ? STORE_PERM_ACC : (A->direct_store ? STORE_DIRECT : STORE_PERM);
   if (A->h.dtype == PJDS_F64) return launch_pjds_dt<double>(A, y, x, s, mode);
   return launch_pjds_dt<float>(A, y, x, s, mode);
+}
+
+int set_cache_policy(int stream_kind, int x_kind) {
+  if (stream_kind < 0 || stream_kind > 3 || x_kind < 0 || x_kind > 3)
+    return set_error(PJDS_ERR_INVALID_ARG, "cache policy kinds: 0 normal, 1 evict_first, 2 evict_last, 3 unchanged");
+  g_pol = stream_kind | (x_kind << 8);
+  return PJDS_OK;
 }
 
 int set_kernel_variant(int r, int u) {

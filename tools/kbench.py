@@ -14,6 +14,7 @@ p.add_argument("--dtypes", default="f64,f32")
 p.add_argument("--fmts", default="pjds32,pjds64,pjds128,ellr")
 p.add_argument("--reps", type=int, default=30)
 p.add_argument("--variants", default="0x0")
+p.add_argument("--policies", default="1x2")
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
@@ -32,9 +33,11 @@ for cfg in a.configs.split(","):
               A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=int(fmt[4:].rstrip("s")), symmetric=sym)
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
-          for var in a.variants.split(","):
+          for var, polk in [(v, q) for v in a.variants.split(",") for q in a.policies.split(",")]:
             vr, vu = map(int, var.split("x"))
             pj.lib().pjds_set_kernel_variant(vr, vu)
+            ps, px = map(int, polk.split("x"))
+            pj.lib().pjds_set_cache_policy(ps, px)
             if fmt == "ellr" and var != a.variants.split(",")[0]: continue
             if a.once:
                 A.spmv(y, x); torch.cuda.synchronize(); continue
@@ -45,7 +48,7 @@ for cfg in a.configs.split(","):
             for _ in range(a.reps): A.spmv(y, x)
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
-            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
                               "stored_bytes": A.info.get("bytes_total")}), flush=True)
           del A
