@@ -115,6 +115,15 @@ class ClockSampler:
                 "reasons": r, "samples": len(self.samples)}
 
 
+def committed_traffic(key: str):
+    """DRAM bytes per launch of the bench kernel from the committed ncu capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f).get(key, {}).get("traffic")
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -179,11 +188,11 @@ def main():
     rp, col, val = g.crs(lo, hi, dtype=npdt)
     nnz_loc = int(rp[-1])
     x_host = inputs.vector(hi - lo, npdt, i0=lo)
-    permuted = world == 1 and a.impl == "pjds" and a.basis == "permuted"
+    permuted = a.impl == "pjds" and a.basis == "permuted"
     compare = {}
     footprint = None
     if world > 1:
-        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows)
+        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=permuted)
         A = None
     else:
         if a.impl == "ellr":
@@ -214,7 +223,7 @@ def main():
     y = torch.empty(hi - lo, dtype=tdt, device=dev)
     if permuted:
         xp = torch.empty_like(x)
-        A.to_permuted(xp, x)  # once, before the "iterative scheme"
+        (D if world > 1 else A).to_permuted(xp, x)  # once, before the "iterative scheme"
         x = xp
     t_setup = time.perf_counter() - t_setup
 
@@ -301,7 +310,7 @@ def main():
 
     if rank == 0:
         wl = f"{a.config}: {CONFIG_DESC[a.config]}, nnz={nnz}, {a.dtype}, {a.impl}"
-        if world == 1 and a.impl == "pjds":
+        if a.impl == "pjds":
             wl += ", permuted basis (PAPER.md L241-246)" if permuted else ", original basis (rows permuted)"
         out = {
             "metric": METRIC,
@@ -315,7 +324,10 @@ def main():
                        "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
             "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": (committed_traffic(f"{a.config}/{a.dtype}/{a.basis}")
+                                     if world == 1 and a.impl == "pjds" else None),
+                         "traffic_source": "profiles/r01_traffic.json (ncu --set full, per launch)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peak_file else "bw probe (this run)",
                          "probe_copy_gbs": round(probe_copy, 1), "probe_read_gbs": round(probe_read, 1),
                          "frac_of_probe_max": round(achieved / max(probe_copy, probe_read), 4),

@@ -201,10 +201,16 @@ enum { PJDS_NO_OVERLAP = 1u /* serialise exchange and compute (vector mode, PAPE
  *                each peer's list in that peer's recv order (ascending)
  *  transport     PJDS_TRANSPORT_*; nccl_unique_id used for NCCL when nranks > 1 (collective call)
  *  block_rows    as pjds_create_from_crs
+ *  flags         0: x_loc / y_loc in the original local order (rows of A_loc permuted only);
+ *                PJDS_PERM_SYMMETRIC: x_loc / y_loc in the local permuted basis of A_loc
+ *                (convert with pjds_dist_permute); every peer list is then
+ *                packed into one message.  All ranks must pass the same flags.
  */
 int pjds_dist_create(pjds_dist_t* out, pjds_plan_t plan, const void* val_loc, int dtype,
                      int32_t block_rows, const int64_t* send_counts, const int32_t* send_cols,
-                     int32_t transport, const void* nccl_unique_id);
+                     int32_t transport, const void* nccl_unique_id, uint32_t flags);
+/* Basis change of a local vector for PJDS_PERM_SYMMETRIC dist handles (see pjds_permute). */
+int pjds_dist_permute(pjds_dist_t D, void* dst, const void* src, int32_t direction, void* stream);
 /* y_loc = A[rows of this rank, :] x ; x_loc / y_loc device pointers of length n_loc. */
 int pjds_dist_spmv(pjds_dist_t D, void* y_loc, const void* x_loc, void* stream, uint32_t flags);
 /* PJDS_TRANSPORT_LOCAL: one call runs all R ranks' spMVMs (same device allowed), D/y/x indexed by rank. */
@@ -214,6 +220,7 @@ typedef struct {
   int64_t n_loc, halo, send_total, packed_send, rows_nonlocal;
   int64_t nnz_local_part, nnz_nonlocal_part;
   int32_t nranks, rank, peers_send, peers_recv, send_messages, recv_messages;
+  int32_t permuted;
 } pjds_dist_info_t;
 int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* out);
 /* The two pJDS parts (owned by D; do not destroy): A_loc, A_nl (A_nl may be NULL if empty). */
@@ -235,7 +242,9 @@ int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gb
    sorted rows per thread (vector loads, R independent FMA chains) and j-unroll `unroll` in {2,4,8}.
    (0, 0) restores the automatic choice.  R is reduced until it divides block_rows.  Every
    variant computes bit-identical y (one FMA chain per row, stored order).  unroll + 16 also
-   enables a tile-wide L2 bulk prefetch of val/col (measured slower; kept for A/B runs). */
+   enables a tile-wide L2 bulk prefetch of val/col (measured slower; kept for A/B runs);
+   rows_per_thread + 8 forces the 64-bit jagged-offset kernels (used when stored + n_pad >= 2^31)
+   on any matrix, so tests can cover them. */
 int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
 
 /* Tuning knob (process-wide): L2 eviction priority of the pJDS kernel's streamed val/col loads

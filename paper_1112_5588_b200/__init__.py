@@ -244,8 +244,10 @@ class DistPjds:
         self.n_loc = self.info["n_loc"]
 
     @classmethod
-    def create(cls, n_global, offsets, rowptr_loc, col_loc, val_loc, block_rows: int = 32, group=None):
-        """Collective over the torch.distributed default (or given) group: one rank per GPU."""
+    def create(cls, n_global, offsets, rowptr_loc, col_loc, val_loc, block_rows: int = 32, group=None,
+               permuted: bool = False):
+        """Collective over the torch.distributed default (or given) group: one rank per GPU.
+        permuted: x_loc / y_loc live in the local permuted basis (to_permuted / from_permuted)."""
         import torch.distributed as dist
         R, rank = dist.get_world_size(group), dist.get_rank(group)
         val_loc = np.ascontiguousarray(val_loc)
@@ -261,13 +263,13 @@ class DistPjds:
             ctypes.memmove(uid, obj[0], 128)
         h = ctypes.c_void_p()
         call("pjds_dist_create", ctypes.byref(h), plan._h, val_loc.ctypes.data, _dt(val_loc), int(block_rows),
-             sc.ctypes.data, scols.ctypes.data, PJDS_TRANSPORT_NCCL, uid)
+             sc.ctypes.data, scols.ctypes.data, PJDS_TRANSPORT_NCCL, uid, PJDS_PERM_SYMMETRIC if permuted else 0)
         info = plan.info
         plan.close()
         return cls(h, info, R, rank, _dt(val_loc))
 
     @classmethod
-    def create_group(cls, n, rowptr, col, val, offsets, block_rows: int = 32):
+    def create_group(cls, n, rowptr, col, val, offsets, block_rows: int = 32, permuted: bool = False):
         """All ranks in THIS process (PJDS_TRANSPORT_LOCAL; halo by device copies) — test harness
         for the split data path on a single GPU.  Returns a list of per-rank handles."""
         rowptr, col, val = _crs(rowptr, col, val)
@@ -293,7 +295,8 @@ class DistPjds:
             v = np.ascontiguousarray(val[rowptr[lo]:rowptr[hi]])
             h = ctypes.c_void_p()
             call("pjds_dist_create", ctypes.byref(h), plans[r]._h, v.ctypes.data, _dt(val), int(block_rows),
-                 sc.ctypes.data, scols.ctypes.data, PJDS_TRANSPORT_LOCAL, None)
+                 sc.ctypes.data, scols.ctypes.data, PJDS_TRANSPORT_LOCAL, None,
+                 PJDS_PERM_SYMMETRIC if permuted else 0)
             out.append(cls(h, plans[r].info, R, r, _dt(val)))
         for p in plans:
             p.close()
@@ -312,6 +315,16 @@ class DistPjds:
              _check_vec(x_loc, self.n_loc, self.dtype, "x"), _stream_ptr(stream),
              PJDS_NO_OVERLAP if no_overlap else 0)
         return y_loc
+
+    def to_permuted(self, dst, src, stream=None):
+        call("pjds_dist_permute", self._h, _check_vec(dst, self.n_loc, self.dtype, "dst"),
+             _check_vec(src, self.n_loc, self.dtype, "src"), 0, _stream_ptr(stream))
+        return dst
+
+    def from_permuted(self, dst, src, stream=None):
+        call("pjds_dist_permute", self._h, _check_vec(dst, self.n_loc, self.dtype, "dst"),
+             _check_vec(src, self.n_loc, self.dtype, "src"), 1, _stream_ptr(stream))
+        return dst
 
     def parts(self):
         a, b = ctypes.c_void_p(), ctypes.c_void_p()

@@ -43,7 +43,7 @@ class DistInfo(ctypes.Structure):
     _fields_ = [("n_loc", c_i64), ("halo", c_i64), ("send_total", c_i64), ("packed_send", c_i64),
                 ("rows_nonlocal", c_i64), ("nnz_local_part", c_i64), ("nnz_nonlocal_part", c_i64),
                 ("nranks", c_i32), ("rank", c_i32), ("peers_send", c_i32), ("peers_recv", c_i32),
-                ("send_messages", c_i32), ("recv_messages", c_i32)]
+                ("send_messages", c_i32), ("recv_messages", c_i32), ("permuted", c_i32)]
 
 
 def struct_dict(s) -> dict:
@@ -68,7 +68,8 @@ _SIGS = {
     "pjds_dist_plan_info": [c_p, c_p],
     "pjds_dist_plan_recv": [c_p, c_p, c_p],
     "pjds_dist_plan_destroy": [c_p],
-    "pjds_dist_create": [c_p, c_p, c_p, ctypes.c_int, c_i32, c_p, c_p, c_i32, c_p],
+    "pjds_dist_create": [c_p, c_p, c_p, ctypes.c_int, c_i32, c_p, c_p, c_i32, c_p, c_u32],
+    "pjds_dist_permute": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_dist_spmv": [c_p, c_p, c_p, c_p, c_u32],
     "pjds_dist_group_spmv": [c_p, c_i32, c_p, c_p, c_p, c_u32],
     "pjds_dist_info": [c_p, c_p],

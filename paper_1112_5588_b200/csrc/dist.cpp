@@ -94,12 +94,6 @@ int nccl_load(const char* path) {
 
 ncclDataType_t nccl_type(int dt) { return dt == PJDS_F64 ? ncclFloat64 : ncclFloat32; }
 
-struct Run {
-  int64_t src;    // sender: local index in x (direct) ; receiver: unused
-  int64_t dst;    // offset in the peer's message space (halo slot / packed offset)
-  int64_t count;
-};
-
 // runs of consecutive values in ids[0..m)
 std::vector<std::pair<int64_t, int64_t>> runs_of(const int32_t* ids, int64_t m) {
   std::vector<std::pair<int64_t, int64_t>> r;  // (first value, length)
@@ -143,6 +137,7 @@ struct pjds_dist {
   cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
   ncclComm_t nccl = nullptr;
   int send_messages = 0, recv_messages = 0;
+  bool permuted = false;
 };
 
 namespace {
@@ -289,9 +284,12 @@ int pjds_dist_plan_destroy(pjds_plan_t P) {
 int pjds_dist_destroy(pjds_dist_t D);
 
 int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype, int32_t block_rows,
-                     const int64_t* send_counts, const int32_t* send_cols, int32_t transport, const void* nccl_id) {
+                     const int64_t* send_counts, const int32_t* send_cols, int32_t transport, const void* nccl_id,
+                     uint32_t flags) {
   if (!out || !P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: NULL argument");
   *out = nullptr;
+  if (flags & ~(uint32_t)PJDS_PERM_SYMMETRIC) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: unknown flags");
+  const bool sym = flags & PJDS_PERM_SYMMETRIC;
   if (dtype != PJDS_F32 && dtype != PJDS_F64) return set_error(PJDS_ERR_INVALID_ARG, "bad dtype");
   if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL)
     return set_error(PJDS_ERR_INVALID_ARG, "bad transport");
@@ -329,7 +327,15 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
     for (size_t k = 0; k < P->nl_src.size(); ++k) std::memcpy(&v_nl[k * vs], vin + P->nl_src[k] * vs, vs);
     D->A_loc = new pjds_mat();
     s = convert_pjds(D->A_loc->h, P->n_loc, P->n_loc, P->loc_rowptr.data(), P->loc_col.data(), v_loc.data(), dtype,
-                     block_rows, false);
+                     block_rows, sym);
+    // local inverse permutation (permuted basis: local row i lives at position inv[i])
+    std::vector<int32_t> inv;
+    if (sym) {
+      inv.resize(P->n_loc);
+      for (int64_t k = 0; k < P->n_loc; ++k) inv[D->A_loc->h.perm[k]] = (int32_t)k;
+      D->A_loc->direct_store = true;
+      D->A_loc->flags = PJDS_PERM_SYMMETRIC;
+    }
     if (s == PJDS_OK) s = upload_pjds(D->A_loc, nullptr);
     if (s != PJDS_OK) return fail(s);
     D->A_loc->ncols = P->n_loc;
@@ -338,10 +344,15 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       D->A_nl = new pjds_mat();
       s = convert_pjds(D->A_nl->h, m, std::max<int64_t>(D->halo, 1), P->nl_rowptr.data(), P->nl_col.data(),
                        v_nl.data(), dtype, block_rows, false);
-      if (s == PJDS_OK) s = upload_pjds(D->A_nl, P->rows_nl.data());  // store to local row rows_nl[perm[k]]
+      // store to local row rows_nl[perm_nl[k]] (or its position in the local permuted basis)
+      std::vector<int32_t> map(P->rows_nl);
+      if (sym)
+        for (auto& r : map) r = inv[r];
+      if (s == PJDS_OK) s = upload_pjds(D->A_nl, map.data());
       if (s != PJDS_OK) return fail(s);
       D->A_nl->ncols = D->halo;
     }
+    D->permuted = sym;
     // ---- send schedule
     int64_t pos = 0;
     for (int q = 0; q < R && send_counts; ++q) {
@@ -349,11 +360,13 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       if (!cnt) continue;
       std::vector<int32_t> ids(cnt);
       for (int64_t i = 0; i < cnt; ++i) ids[i] = (int32_t)(send_cols[pos + i] - P->lo);
+      if (sym)
+        for (auto& v : ids) v = inv[v];  // gather from x in the local permuted basis
       pos += cnt;
       auto runs = runs_of(ids.data(), cnt);
       pjds_dist::PeerSend ps;
       ps.peer = q;
-      if ((int)runs.size() <= kMaxRuns) {
+      if (!sym && (int)runs.size() <= kMaxRuns) {
         ps.packed = false;
         ps.runs = runs;
       } else {
@@ -373,7 +386,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       auto runs = runs_of(P->recv_cols.data() + hoff, cnt);
       pjds_dist::PeerRecv pr;
       pr.peer = q;
-      if ((int)runs.size() <= kMaxRuns) {
+      if (!sym && (int)runs.size() <= kMaxRuns) {  // permuted basis: one packed message per peer
         int64_t o = hoff;
         for (auto& r : runs) {
           pr.runs.push_back({o, r.second});
@@ -438,7 +451,13 @@ int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* o) {
   o->nranks = D->R; o->rank = D->rank;
   o->peers_send = (int32_t)D->sends.size(); o->peers_recv = (int32_t)D->recvs.size();
   o->send_messages = D->send_messages; o->recv_messages = D->recv_messages;
+  o->permuted = D->permuted;
   return PJDS_OK;
+}
+
+int pjds_dist_permute(pjds_dist_t D, void* dst, const void* src, int32_t direction, void* stream) {
+  if (!D) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_permute: NULL handle");
+  return pjds_permute(D->A_loc, dst, src, direction, stream);
 }
 
 int pjds_dist_parts(pjds_dist_t D, pjds_t* a, pjds_t* b) {

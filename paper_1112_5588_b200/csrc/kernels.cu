@@ -273,6 +273,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode)
 
 // kernel variant (rows per thread R, j-unroll U); 0 = automatic choice
 static int g_var_r = 0, g_var_u = 0;
+static bool g_force_off64 = false;  // test hook: exercise the 64-bit offset kernels on small inputs
 
 template <typename T, typename Off>
 int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode) {
@@ -295,7 +296,7 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
 
 template <typename T>
 int launch_pjds_dt(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode) {
-  const bool off32 = A->h.stored + A->h.n_pad < (int64_t(1) << 31);
+  const bool off32 = !g_force_off64 && A->h.stored + A->h.n_pad < (int64_t(1) << 31);
   if (off32) return launch_pjds_off<T, int32_t>(A, y, x, s, mode);
   return launch_pjds_off<T, int64_t>(A, y, x, s, mode);
 }
@@ -397,11 +398,14 @@ int set_kernel_variant(int r, int u) {
   // u >= 16 encodes "with the tile-wide L2 bulk prefetch" (u - 16) for A/B measurements
   const bool pf = u >= 16;
   if (u >= 16) u -= 16;
+  const bool off64 = r >= 8;  // rows_per_thread + 8: force 64-bit jagged offsets
+  if (r >= 8) r -= 8;
   if (!((r == 0 && u == 0) || ((r == 1 || r == 2 || r == 4) && (u == 2 || u == 4 || u == 8))))
     return set_error(PJDS_ERR_INVALID_ARG, "variant: rows_per_thread in {1,2,4}, unroll in {2,4,8} (or 0,0)");
   g_var_r = r;
   g_var_u = u;
   g_prefetch = pf;
+  g_force_off64 = off64;
   return PJDS_OK;
 }
 

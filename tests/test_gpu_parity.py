@@ -168,15 +168,20 @@ def test_symmetric_mode(pj):
 
 
 @pytest.mark.parametrize("R", [1, 2, 3, 4, 8])
-def test_dist_group_random(pj, R):
+@pytest.mark.parametrize("permuted", [False, True])
+def test_dist_group_random(pj, R, permuted):
     n = 4000
     _, rp, col, val = inputs.small("random", n, seed=R, max=50)
     x = inputs.vector(n)
     offs = np.array([n * r // R for r in range(R + 1)], np.int64)
-    hs = pj.DistPjds.create_group(n, rp, col, val, offs)
+    hs = pj.DistPjds.create_group(n, rp, col, val, offs, permuted=permuted)
     xs = [tdev(x[offs[r]:offs[r + 1]]) for r in range(R)]
+    if permuted:
+        xs = [h.to_permuted(torch.empty_like(v), v) for h, v in zip(hs, xs)]
     ys = [torch.full((offs[r + 1] - offs[r],), float("nan"), dtype=torch.float64, device="cuda") for r in range(R)]
     pj.DistPjds.group_spmv(hs, ys, xs)
+    if permuted:
+        ys = [h.from_permuted(torch.empty_like(v), v) for h, v in zip(hs, ys)]
     torch.cuda.synchronize()
     y = np.concatenate([t.cpu().numpy() for t in ys])
     ref = odist.spmv(odist.split(n, rp, col, val, offs), x)
@@ -184,19 +189,24 @@ def test_dist_group_random(pj, R):
     check_y(y, n, rp, col, val, x, exact=(R == 1))
 
 
-@pytest.mark.parametrize("name,R", [("C1", 4), ("C3", 4), ("C3", 8)])
-def test_dist_group_configs(pj, name, R):
+@pytest.mark.parametrize("name,R,permuted", [("C1", 4, False), ("C1", 4, True), ("C3", 4, False), ("C3", 8, True)])
+def test_dist_group_configs(pj, name, R, permuted):
     n, rp, col, val = inputs.config_crs(name)
     x = inputs.vector(n)
     blk = 1024 if name == "C1" else 15504
     nb = n // blk
     offs = np.array([(nb * r // R) * blk for r in range(R + 1)], np.int64)
-    hs = pj.DistPjds.create_group(n, rp, col, val, offs)
+    hs = pj.DistPjds.create_group(n, rp, col, val, offs, permuted=permuted)
     for h in hs:
-        assert h.info["packed_send"] == 0  # HMEp halos are whole segments: sent straight from x
+        if not permuted:
+            assert h.info["packed_send"] == 0  # HMEp halos are whole segments: sent straight from x
     xs = [tdev(x[offs[r]:offs[r + 1]]) for r in range(R)]
+    if permuted:
+        xs = [h.to_permuted(torch.empty_like(v), v) for h, v in zip(hs, xs)]
     ys = [torch.empty(int(offs[r + 1] - offs[r]), dtype=torch.float64, device="cuda") for r in range(R)]
     pj.DistPjds.group_spmv(hs, ys, xs)
+    if permuted:
+        ys = [h.from_permuted(torch.empty_like(v), v) for h, v in zip(hs, ys)]
     torch.cuda.synchronize()
     y = np.concatenate([t.cpu().numpy() for t in ys])
     check_y(y, n, rp, col, val, x, exact=False)
@@ -222,10 +232,11 @@ def test_misuse_errors(pj):
         A.spmv(torch.empty(n, dtype=torch.float32, device="cuda"), x)
 
 
-@pytest.mark.parametrize("variant", [(1, 8), (2, 4), (2, 8), (4, 2), (4, 4)])
+@pytest.mark.parametrize("variant", [(1, 8), (2, 4), (2, 8), (4, 2), (4, 4), (9, 8), (10, 4), (12, 2), (4, 18)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_kernel_variants_bitwise(pj, variant, dtype):
-    """Every (rows per thread, unroll) variant gives the same per-row FMA chain."""
+    """Every (rows per thread, unroll) variant gives the same per-row FMA chain (R+8: 64-bit offsets,
+    U+16: with the L2 bulk prefetch)."""
     L = pj.lib()
     try:
         assert L.pjds_set_kernel_variant(*variant) == 0
