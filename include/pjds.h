@@ -252,6 +252,13 @@ int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
    Default (1, 2).  Results are unaffected. */
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind);
 
+/* Tuning knob (process-wide): execution order of the pJDS kernel's CTA tiles.  0 = storage
+   order (longest blocks first); 1 = tiles ordered by the original index of their first row, so
+   rows of all length classes from one region of the matrix run together (RHS reuse in L2,
+   local y stores); 2 = auto (default): 1 in the row-only basis or when x exceeds 64 MB, else 0.
+   The per-row arithmetic, and therefore y, is identical. */
+int pjds_set_tile_order(int32_t mode);
+
 /* Number of kernel launches this library has enqueued (process-wide counter). */
 int64_t pjds_launch_count(void);
 

@@ -80,6 +80,7 @@ _SIGS = {
     "pjds_bw_probe": [c_i64, c_i32, c_p, c_p],
     "pjds_set_kernel_variant": [c_i32, c_i32],
     "pjds_set_cache_policy": [c_i32, c_i32],
+    "pjds_set_tile_order": [c_i32],
 }
 EXPORTED = sorted(list(_SIGS) + ["pjds_launch_count", "pjds_last_error", "pjds_version"])
 

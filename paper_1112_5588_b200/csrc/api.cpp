@@ -23,6 +23,10 @@ static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
 int free_pjds_device(pjds_mat* A) {
   cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
   cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys);
+  for (auto& o : A->d_order) {
+    cudaFree(o);
+    o = nullptr;
+  }
   A->d_val = A->d_xs = A->d_ys = nullptr;
   A->d_col = A->d_block_len = A->d_perm = nullptr;
   A->d_col_start = nullptr;
@@ -275,6 +279,7 @@ int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll) {
 }
 
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind) { return set_cache_policy(stream_kind, x_kind); }
+int pjds_set_tile_order(int32_t mode) { return set_tile_order(mode); }
 
 int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs) {
   if (!copy_gbs || !read_gbs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_bw_probe: NULL argument");

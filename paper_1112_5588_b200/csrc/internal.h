@@ -71,6 +71,7 @@ struct pjds_mat {
   void* d_ys = nullptr;
   int64_t ncols = 0;
   bool direct_store = false;  // permuted basis: y[k] stored contiguously, perm not read
+  int32_t* d_order[3] = {nullptr, nullptr, nullptr};  // CTA tile execution orders (R = 1, 2, 4)
 };
 
 struct ellr_mat {
@@ -94,6 +95,7 @@ int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, i
 int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int dtype, cudaStream_t s);
 int set_kernel_variant(int r, int u);
 int set_cache_policy(int stream_kind, int x_kind);
+int set_tile_order(int mode);
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
 void count_launch(int64_t k = 1);
 }  // namespace pjds

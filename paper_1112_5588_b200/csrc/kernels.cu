@@ -17,6 +17,8 @@
 #include <atomic>
 #include <cstdio>
 #include <algorithm>
+#include <climits>
+#include <vector>
 #include "internal.h"
 
 namespace pjds {
@@ -153,11 +155,13 @@ template <typename T, typename Off, int R, int U, int MODE, bool PF>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
-                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol) {
+                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order) {
   __shared__ Off s_cs[kSmemCS];
-  const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  // execution order of the CTA tiles (storage order, or by original row; results are identical)
+  const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
+  const int64_t t = tile * kThreads + threadIdx.x;
   const int64_t k0 = t * R;
-  const int64_t cta_k0 = (int64_t)blockIdx.x * kThreads * R;
+  const int64_t cta_k0 = tile * kThreads * R;
   const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
   const int lim = min(cta_len + 1, kSmemCS);
   for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
@@ -243,6 +247,35 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 }
 
 static int g_pol = 1 | (2 << 8);  // val/col evict_first, x evict_last
+static int g_tile_order = 2;  // 0 storage order, 1 by first row's original index, 2 auto (see launch_pjds_t)
+
+// Tiles (CTAs of rows_per_tile consecutive sorted rows) ordered by the original index of their first
+// row: all length classes of one region of the original matrix run together, so the RHS entries
+// they share are reused from L2 (the sort destroys this locality).
+int tile_order_for(pjds_mat* A, int R, int64_t rows_per_tile, int64_t tiles, const int** out) {
+  int slot = R == 4 ? 2 : (R == 2 ? 1 : 0);
+  if (!A->d_order[slot]) {
+    const auto& h = A->h;
+    std::vector<int64_t> key(tiles);
+    for (int64_t t = 0; t < tiles; ++t) {
+      const int64_t k = t * rows_per_tile;
+      key[t] = k < h.n ? (int64_t)h.perm[k] : INT64_MAX;
+    }
+    std::vector<int32_t> ord(tiles);
+    for (int64_t t = 0; t < tiles; ++t) ord[t] = (int32_t)t;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_order[slot], tiles * 4));
+    PJDS_CUDA_TRY(cudaMemcpy(A->d_order[slot], ord.data(), tiles * 4, cudaMemcpyHostToDevice));
+  }
+  *out = A->d_order[slot];
+  return PJDS_OK;
+}
+
+int set_tile_order_impl(int mode) {
+  if (mode < 0 || mode > 2) return set_error(PJDS_ERR_INVALID_ARG, "tile order: 0 storage, 1 original-row, 2 auto");
+  g_tile_order = mode;
+  return PJDS_OK;
+}
 static bool g_prefetch = false;  // measured: the tile-wide L2 bulk prefetch slows every config
 
 template <typename T, typename Off, int R, int U>
@@ -251,9 +284,16 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode)
   const int64_t threads = h.n_pad / R;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
+  const int* order = nullptr;
+  // auto: original-row order when y is scattered through perm (keeps the stores of a region
+  // together) or when x does not fit comfortably in L2 (measured: C5 DP permuted +6 %, rows-only
+  // +44 %; C2/C4, whose x fits L2, lose ~1 % with it, so they keep storage order)
+  const bool by_row = g_tile_order == 1 ||
+                      (g_tile_order == 2 && (mode != STORE_DIRECT || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
+  if (by_row) PJDS_TRY(tile_order_for(const_cast<pjds_mat*>(A), R, kThreads * R, grid, &order));
 #define PJDS_LAUNCH_PF(M, PF)                                                                            \
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
-      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol)
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order)
 #define PJDS_LAUNCH(M)             \
   if (g_prefetch) PJDS_LAUNCH_PF(M, true); \
   else PJDS_LAUNCH_PF(M, false)
@@ -386,6 +426,8 @@ int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, 
   if (A->h.dtype == PJDS_F64) return launch_pjds_dt<double>(A, y, x, s, mode);
   return launch_pjds_dt<float>(A, y, x, s, mode);
 }
+
+int set_tile_order(int mode) { return set_tile_order_impl(mode); }
 
 int set_cache_policy(int stream_kind, int x_kind) {
   if (stream_kind < 0 || stream_kind > 3 || x_kind < 0 || x_kind > 3)

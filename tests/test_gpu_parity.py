@@ -275,3 +275,21 @@ def test_permute_and_symmetric_host_e2e(pj):
     y = np.empty(n)
     A.spmv_host(y, x)
     check_y(y, n, rp, col, val, x)
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+def test_tile_order_bitwise(pj, order):
+    """CTA execution order does not change any row's chain."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_tile_order(order) == 0
+        for name in ("C1", "C4"):
+            n, rp, col, val = inputs.config_crs(name)
+            x = inputs.vector(n)
+            for sym in (False, True):
+                A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=sym)
+                y = np.empty(n)
+                A.spmv_host(y, x)
+                check_y(y, n, rp, col, val, x)
+    finally:
+        L.pjds_set_tile_order(2)

@@ -15,6 +15,7 @@ p.add_argument("--fmts", default="pjds32,pjds64,pjds128,ellr")
 p.add_argument("--reps", type=int, default=30)
 p.add_argument("--variants", default="0x0")
 p.add_argument("--policies", default="1x2")
+p.add_argument("--orders", default="2")
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
@@ -33,7 +34,8 @@ for cfg in a.configs.split(","):
               A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=int(fmt[4:].rstrip("s")), symmetric=sym)
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
-          for var, polk in [(v, q) for v in a.variants.split(",") for q in a.policies.split(",")]:
+          for var, polk, order in [(v, q, o) for v in a.variants.split(",") for q in a.policies.split(",") for o in a.orders.split(",")]:
+            pj.lib().pjds_set_tile_order(int(order))
             vr, vu = map(int, var.split("x"))
             pj.lib().pjds_set_kernel_variant(vr, vu)
             ps, px = map(int, polk.split("x"))
@@ -48,7 +50,7 @@ for cfg in a.configs.split(","):
             for _ in range(a.reps): A.spmv(y, x)
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
-            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
                               "stored_bytes": A.info.get("bytes_total")}), flush=True)
           del A
