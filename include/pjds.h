@@ -231,6 +231,28 @@ int pjds_dist_destroy(pjds_dist_t D);
 int pjds_nccl_load(const char* libpath);
 int pjds_nccl_unique_id(void* out128);
 
+/* ------------------------------------------------------------------ eigensolver driver */
+
+/*
+ * pjds_lanczos — m steps of the symmetric Lanczos recurrence, the eigensolver usage the paper's
+ * HMEp matrix comes from, on a PJDS_PERM_SYMMETRIC handle, entirely
+ * in the permuted basis:
+ *   v_0 = v0/||v0||; w = A v_j; alpha_j = w.v_j; w -= alpha_j v_j + beta_{j-1} v_{j-1};
+ *   beta_j = ||w||; v_{j+1} = w / beta_j.
+ * Precondition: A symmetric (not checked).  v0: device vector (permuted basis, handle dtype, n
+ * entries, not modified).  alpha[m], beta[m]: host outputs (double).  *steps_done = m, or j+1 if
+ * beta_j = 0 (invariant subspace).  Dot products accumulate in double.  The m iterations (pJDS
+ * kernel + 2 fused vector passes + 2 one-CTA reductions each) are captured into one CUDA graph and
+ * launched on `stream`; the call synchronises `stream`.  Work buffers (3 vectors) are allocated
+ * and freed inside.
+ */
+int pjds_lanczos(pjds_t A, const void* v0, int32_t m, double* alpha, double* beta,
+                 int32_t* steps_done, void* stream);
+
+/* Eigenvalues (ascending) of the m x m symmetric tridiagonal matrix with diagonal alpha[m] and
+   off-diagonal beta[m-1] (the Ritz values of pjds_lanczos), by Sturm bisection; host only. */
+int pjds_tridiag_eigenvalues(int32_t m, const double* alpha, const double* beta, double* evals);
+
 /* ------------------------------------------------------------------ misc */
 
 /* Stream-bandwidth probe (roofline denominator, measured in the same run): copies / reads

@@ -96,8 +96,9 @@ class Generator:
         _load().pjdsgen_rowlen(self._h, r0, r1, out.ctypes.data)
         return out
 
-    def crs(self, r0: int = 0, r1: int | None = None, dtype=np.float64):
-        """Rows [r0, r1) as CRS: (rowptr int64 [m+1], col int32 (global ids), val dtype)."""
+    def crs(self, r0: int = 0, r1: int | None = None, dtype=np.float64, symmetric: bool = False):
+        """Rows [r0, r1) as CRS: (rowptr int64 [m+1], col int32 (global ids), val dtype).
+        symmetric: a(r,c) = a(c,r) (structurally symmetric families: HMEp, banded, sAMG)."""
         r1 = self.n if r1 is None else r1
         lens = self.rowlen(r0, r1)
         rowptr = np.zeros(r1 - r0 + 1, dtype=np.int64)
@@ -107,7 +108,7 @@ class Generator:
         dt = np.dtype(dtype)
         val = np.empty(nnz, dtype=dt)
         _load().pjdsgen_fill(self._h, r0, r1, rowptr.ctypes.data, col.ctypes.data, val.ctypes.data,
-                             1 if dt == np.float64 else 0)
+                             (1 if dt == np.float64 else 0) | (2 if symmetric else 0))
         return rowptr, col, val
 
 
@@ -123,9 +124,9 @@ def value(row: int, col: int, seed: int = BASE_SEED) -> float:
     return float(_load().pjdsgen_value(seed, row, col))
 
 
-def config_crs(name: str, dtype=np.float64, seed: int = BASE_SEED):
+def config_crs(name: str, dtype=np.float64, seed: int = BASE_SEED, symmetric: bool = False):
     g = Generator.from_config(name, seed)
-    rowptr, col, val = g.crs(dtype=dtype)
+    rowptr, col, val = g.crs(dtype=dtype, symmetric=symmetric)
     return g.n, rowptr, col, val
 
 

@@ -414,8 +414,12 @@ int64_t pjdsgen_rowlen(void* h, int64_t r0, int64_t r1, int32_t* len) {
 }
 
 // Fill rows [r0, r1) given rowptr (length r1-r0+1, rowptr[0] = 0): ascending global column ids
-// and values.  dtype 0 = float32 (rounded from the double value), 1 = float64.
+// and values.  dtype 0 = float32 (rounded from the double value), 1 = float64; +2 = symmetric
+// values a(r,c) = a(c,r) (hash of the unordered pair; every family's pattern is structurally
+// symmetric except DLR1's k-NN blocks).
 void pjdsgen_fill(void* h, int64_t r0, int64_t r1, const int64_t* rowptr, int32_t* col, void* val, int dtype) {
+  const bool sym = dtype & 2;
+  dtype &= 1;
   const Gen& g = *(Gen*)h;
 #pragma omp parallel for schedule(static, 4096)
   for (int64_t r = r0; r < r1; ++r) {
@@ -424,7 +428,9 @@ void pjdsgen_fill(void* h, int64_t r0, int64_t r1, const int64_t* rowptr, int32_
     int64_t o = rowptr[r - r0];
     for (int i = 0; i < k; ++i) {
       col[o + i] = cols[i];
-      double v = unit_pm1(hash3(g.seed, (uint64_t)r, (uint64_t)cols[i]));
+      const uint64_t a = sym ? (uint64_t)std::min<int64_t>(r, cols[i]) : (uint64_t)r;
+      const uint64_t b = sym ? (uint64_t)std::max<int64_t>(r, cols[i]) : (uint64_t)cols[i];
+      double v = unit_pm1(hash3(g.seed, a, b));
       if (dtype == 1) ((double*)val)[o + i] = v;
       else ((float*)val)[o + i] = (float)v;
     }

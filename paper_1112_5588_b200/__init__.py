@@ -121,6 +121,16 @@ class PjdsMatrix:
         call("pjds_spmv_host", self._h, y.ctypes.data, x.ctypes.data, _stream_ptr(stream))
         return y
 
+    def lanczos(self, v0, m: int, stream=None):
+        """m Lanczos steps in the permuted basis (needs symmetric=True and a symmetric matrix).
+        v0: CUDA tensor in the permuted basis.  Returns (alpha, beta, steps_done) as numpy."""
+        alpha = np.zeros(m)
+        beta = np.zeros(m)
+        steps = ctypes.c_int32()
+        call("pjds_lanczos", self._h, _check_vec(v0, self.n, self.dtype, "v0"), int(m), alpha.ctypes.data,
+             beta.ctypes.data, ctypes.byref(steps), _stream_ptr(stream))
+        return alpha, beta, steps.value
+
     def histogram(self):
         counts = np.zeros(self.info["len_max"] + 1, dtype=np.int64)
         call("pjds_histogram", self._h, counts.ctypes.data, len(counts))
@@ -348,3 +358,12 @@ def bw_probe(nbytes: int = 4 << 30, reps: int = 5):
     c, r = ctypes.c_double(), ctypes.c_double()
     call("pjds_bw_probe", int(nbytes), int(reps), ctypes.byref(c), ctypes.byref(r))
     return c.value, r.value
+
+
+def tridiag_eigenvalues(alpha, beta):
+    """Ritz values: ascending eigenvalues of tridiag(beta, alpha, beta) (library bisection)."""
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    b = np.ascontiguousarray(beta, dtype=np.float64)
+    ev = np.zeros(len(a))
+    call("pjds_tridiag_eigenvalues", len(a), a.ctypes.data, b.ctypes.data, ev.ctypes.data)
+    return ev

@@ -81,6 +81,8 @@ _SIGS = {
     "pjds_set_kernel_variant": [c_i32, c_i32],
     "pjds_set_cache_policy": [c_i32, c_i32],
     "pjds_set_tile_order": [c_i32],
+    "pjds_lanczos": [c_p, c_p, c_i32, c_p, c_p, c_p, c_p],
+    "pjds_tridiag_eigenvalues": [c_i32, c_p, c_p, c_p],
 }
 EXPORTED = sorted(list(_SIGS) + ["pjds_launch_count", "pjds_last_error", "pjds_version"])
 

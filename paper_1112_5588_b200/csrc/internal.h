@@ -90,6 +90,9 @@ int free_pjds_device(pjds_mat* A);
 
 // ---- kernel launchers (kernels.cu) -----------------------------------------------------------
 int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool accumulate);
+// y = A x (permuted basis) plus per-CTA partials of y.x into part[0 .. *nparts); part must hold
+// n_pad / 256 + 1 doubles (the largest grid of any variant)
+int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t s, double* part, int64_t* nparts);
 int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s);
 int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, int dtype, int back, cudaStream_t s);
 int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int dtype, cudaStream_t s);

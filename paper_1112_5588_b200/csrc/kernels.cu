@@ -136,7 +136,9 @@ constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
 
 // Store modes: y[perm[k]] = acc (row-only basis), y[k] = acc (permuted basis, PJDS_PERM_SYMMETRIC),
 // y[perm[k]] += acc (dist nonlocal part: the result is written twice).
-enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2 };
+// STORE_DIRECT_DOT additionally writes per-CTA partial sums of y[k]*x[k] (permuted basis, so x[k]
+// is the input entry of row k): the Lanczos alpha = (A v).v fused into the product's epilogue.
+enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 3 };
 
 // ---- pJDS kernel -----------------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
@@ -155,7 +157,8 @@ template <typename T, typename Off, int R, int U, int MODE, bool PF>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
-                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order) {
+                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
+                 double* __restrict__ dot_part) {
   __shared__ Off s_cs[kSmemCS];
   // execution order of the CTA tiles (storage order, or by original row; results are identical)
   const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
@@ -166,7 +169,12 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const int lim = min(cta_len + 1, kSmemCS);
   for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
   __syncthreads();
-  if (k0 >= n_pad) return;
+  const bool active = k0 < n_pad;
+  if (!active && MODE != STORE_DIRECT_DOT) return;
+  T acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = T(0);
+  if (active) {
   const int64_t warp_k0 = (t & ~int64_t(31)) * R;
   const int wlen = block_len[warp_k0 / br];
   const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
@@ -186,9 +194,6 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
     }
     __syncwarp();
   }
-  T acc[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = T(0);
   int j = 0;
   for (; j + U <= len; j += U) {  // full chunks: no predicates, all U loads issued back to back
     Vec<T, R> v[U];
@@ -235,13 +240,30 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   for (int r = 0; r < R; ++r) {
     const int64_t k = k0 + r;
     if (k < n) {
-      if (MODE == STORE_DIRECT) {
+      if (MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) {
         y[k] = acc[r];
       } else {
         const int p = perm[k];
         if (MODE == STORE_PERM_ACC) y[p] = y[p] + acc[r];
         else y[p] = acc[r];
       }
+    }
+  }
+  }  // active
+  if (MODE == STORE_DIRECT_DOT) {
+    __shared__ double s_red[kThreads / 32];
+    double d = 0.0;
+    if (active)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (k0 + r < n) d = fma((double)acc[r], (double)x[k0 + r], d);
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tsum = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) tsum += s_red[w];
+      dot_part[blockIdx.x] = tsum;
     }
   }
 }
@@ -279,26 +301,29 @@ int set_tile_order_impl(int mode) {
 static bool g_prefetch = false;  // measured: the tile-wide L2 bulk prefetch slows every config
 
 template <typename T, typename Off, int R, int U>
-int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode) {
+int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part, int64_t* nparts) {
   const auto& h = A->h;
   const int64_t threads = h.n_pad / R;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
+  if (nparts) *nparts = grid;
   if (grid == 0) return PJDS_OK;
   const int* order = nullptr;
   // auto: original-row order when y is scattered through perm (keeps the stores of a region
   // together) or when x does not fit comfortably in L2 (measured: C5 DP permuted +6 %, rows-only
   // +44 %; C2/C4, whose x fits L2, lose ~1 % with it, so they keep storage order)
   const bool by_row = g_tile_order == 1 ||
-                      (g_tile_order == 2 && (mode != STORE_DIRECT || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
+                      (g_tile_order == 2 && (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(const_cast<pjds_mat*>(A), R, kThreads * R, grid, &order));
 #define PJDS_LAUNCH_PF(M, PF)                                                                            \
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
-      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order)
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part)
 #define PJDS_LAUNCH(M)             \
   if (g_prefetch) PJDS_LAUNCH_PF(M, true); \
   else PJDS_LAUNCH_PF(M, false)
   if (mode == STORE_DIRECT) {
     PJDS_LAUNCH(STORE_DIRECT);
+  } else if (mode == STORE_DIRECT_DOT) {
+    PJDS_LAUNCH(STORE_DIRECT_DOT);
   } else if (mode == STORE_PERM_ACC) {
     PJDS_LAUNCH(STORE_PERM_ACC);
   } else {
@@ -316,7 +341,7 @@ static int g_var_r = 0, g_var_u = 0;
 static bool g_force_off64 = false;  // test hook: exercise the 64-bit offset kernels on small inputs
 
 template <typename T, typename Off>
-int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode) {
+int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode, double* dp, int64_t* np) {
   int R = g_var_r, U = g_var_u;
   if (R == 0) {
     // enough warps to cover the SMs several times: R = 4 (256-bit DP loads) for large matrices,
@@ -329,22 +354,28 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;
   const T* xx = (const T*)x;
-  if (R == 4) return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode) : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode);
-  if (R == 2) return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode) : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode);
-  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode);
+  if (R == 4)
+    return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np)
+                  : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode, dp, np);
+  if (R == 2)
+    return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np)
+                  : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode, dp, np);
+  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode, dp, np);
 }
 
 template <typename T>
-int launch_pjds_dt(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode) {
+int launch_pjds_dt(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode, double* dp = nullptr,
+                   int64_t* np = nullptr) {
   const bool off32 = !g_force_off64 && A->h.stored + A->h.n_pad < (int64_t(1) << 31);
-  if (off32) return launch_pjds_off<T, int32_t>(A, y, x, s, mode);
-  return launch_pjds_off<T, int64_t>(A, y, x, s, mode);
+  if (off32) return launch_pjds_off<T, int32_t>(A, y, x, s, mode, dp, np);
+  return launch_pjds_off<T, int64_t>(A, y, x, s, mode, dp, np);
 }
 
 // ---- ELLPACK-R kernel ------------------------------------------------------------------------
 // Consecutive rows to consecutive threads, R consecutive rows per thread with
 // vector loads of val[j*N_pad + i .. +R-1]; each row stops at its own rowmax[i] ("threads only
-// execute non-zero contributions", L187-191) while the warp runs to its longest row.
+// execute non-zero contributions", L187-191); lanes of a warp diverge at the tail, so the warp
+// stays resident until its longest row is done (the "hardware reservation" of Fig. 2b).
 template <typename T, int R, int U>
 __global__ void __launch_bounds__(kThreads)
 ellr_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int* __restrict__ rowmax,
@@ -358,6 +389,8 @@ ellr_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   int tmax = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) tmax = max(tmax, lens.v[r]);
+  // one predicated loop to the warp's longest row keeps the lanes converged; measured faster than
+  // an unpredicated per-thread main loop + tail (which diverges inside mixed-length warps)
   const int wmax = __reduce_max_sync(__activemask(), tmax);
   T acc[R];
 #pragma unroll
@@ -427,6 +460,12 @@ int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, 
   return launch_pjds_dt<float>(A, y, x, s, mode);
 }
 
+int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t s, double* part, int64_t* nparts) {
+  if (!A->direct_store) return set_error(PJDS_ERR_INVALID_ARG, "fused dot needs the permuted basis");
+  if (A->h.dtype == PJDS_F64) return launch_pjds_dt<double>(A, y, x, s, STORE_DIRECT_DOT, part, nparts);
+  return launch_pjds_dt<float>(A, y, x, s, STORE_DIRECT_DOT, part, nparts);
+}
+
 int set_tile_order(int mode) { return set_tile_order_impl(mode); }
 
 int set_cache_policy(int stream_kind, int x_kind) {
@@ -451,20 +490,33 @@ int set_kernel_variant(int r, int u) {
   return PJDS_OK;
 }
 
-int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
+template <typename T, int R, int U>
+int launch_ellr_t(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
   const auto& h = A->h;
-  constexpr int R = 2, U = 4;
   const int64_t grid = (h.n_pad / R + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
-  if (h.dtype == PJDS_F64)
-    ellr_spmv_kernel<double, R, U><<<(unsigned)grid, kThreads, 0, s>>>((const double*)A->d_val, A->d_col, A->d_rowmax,
-                                                                       (const double*)x, (double*)y, h.n, h.n_pad);
-  else
-    ellr_spmv_kernel<float, R, U><<<(unsigned)grid, kThreads, 0, s>>>((const float*)A->d_val, A->d_col, A->d_rowmax,
-                                                                     (const float*)x, (float*)y, h.n, h.n_pad);
+  ellr_spmv_kernel<T, R, U><<<(unsigned)grid, kThreads, 0, s>>>((const T*)A->d_val, A->d_col, A->d_rowmax,
+                                                                (const T*)x, (T*)y, h.n, h.n_pad);
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;
+}
+
+template <typename T>
+int launch_ellr_dt(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
+  int R = g_var_r;
+  if (R == 0) {  // same rule as the pJDS kernel (measured: R=4,U=2 best on C2/C3/C5 in SP and DP)
+    const int64_t np = A->h.n_pad;
+    R = np / 4 >= (int64_t(1) << 19) ? 4 : (np / 2 >= (int64_t(1) << 17) ? 2 : 1);
+  }
+  if (R == 4) return launch_ellr_t<T, 4, 2>(A, y, x, s);
+  if (R == 2) return launch_ellr_t<T, 2, 4>(A, y, x, s);
+  return launch_ellr_t<T, 1, 8>(A, y, x, s);
+}
+
+int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
+  if (A->h.dtype == PJDS_F64) return launch_ellr_dt<double>(A, y, x, s);
+  return launch_ellr_dt<float>(A, y, x, s);
 }
 
 int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, int dtype, int back, cudaStream_t s) {

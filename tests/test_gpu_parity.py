@@ -255,6 +255,11 @@ def test_kernel_variants_bitwise(pj, variant, dtype):
                     yo[perm] = yh
                     yh = yo
                 check_y(yh, n, rp, col, val, x)
+            E = pj.EllrMatrix.from_crs(n, rp, col, val)  # the variant knob also picks ELLPACK-R's R
+            y = torch.full((n,), float("nan"), dtype=torch.float64 if dtype == np.float64 else torch.float32,
+                           device="cuda")
+            E.spmv(y, tdev(x))
+            check_y(y.cpu().numpy(), n, rp, col, val, x)
     finally:
         L.pjds_set_kernel_variant(0, 0)
 
