@@ -165,6 +165,7 @@ def main():
     import torch
     import inputs
     import paper_1112_5588_b200 as pj
+    from paper_1112_5588_b200 import perfmodel
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -297,6 +298,7 @@ def main():
     # end-to-end through the public API with host buffers in the original basis (H2D x, basis
     # change, kernel, basis change back, D2H y, every step)
     e2e = None
+    model = None
     if world == 1 and a.impl == "pjds":
         xh = torch.from_numpy(x_host).pin_memory().numpy()
         yh = torch.empty(n, dtype=tdt).pin_memory().numpy()
@@ -304,6 +306,22 @@ def main():
         te = timed(lambda: A.spmv_host(yh, xh), a.e2e_steps) * 1e-3
         e2e = {"value": round(2.0 * nnz / te / 1e9, 2), "unit": "GFlop/s", "h2d_bytes_per_step": n * sv,
                "d2h_bytes_per_step": n * sv, "ms_per_step": round(te * 1e3, 3)}
+        # the paper's PCIe model (Eq. 2-4) with this box's measured bandwidths:
+        # B_PCI from the e2e transfer time, B_GPU = the read probe
+        t_pci_meas = max(te - t_s, 1e-9)
+        b_pci = 2 * n * sv / t_pci_meas
+        ratio = max(probe_copy, probe_read) * 1e9 / b_pci
+        traffic = committed_traffic(f"{a.config}/{a.dtype}/{a.basis}")
+        alpha = (perfmodel.measured_alpha(traffic - n * sv, A.info["stored"], nnz, n, sv,
+                                          aux_bytes=A.info["bytes_aux"] - A.info["n"] * 4 * permuted)
+                 if traffic else None)
+        model = {"B_pci_GBs": round(b_pci / 1e9, 1), "B_gpu_over_B_pci": round(ratio, 1),
+                 "alpha_measured": round(alpha, 4) if alpha is not None else None,
+                 "alpha_ideal": round(n / nnz, 4),
+                 "eq3_nnzr_upper_50pct_penalty": round(perfmodel.n_nzr_upper(ratio, alpha or perfmodel.RECIPROCAL), 1),
+                 "eq4_nnzr_lower_10pct_penalty": round(perfmodel.n_nzr_lower(ratio, alpha or perfmodel.RECIPROCAL), 1),
+                 "n_nzr": round(nnz / n, 2),
+                 "pci_share_of_e2e": round(t_pci_meas / te, 3)}
     elif world > 1:
         e2e = {"value": None, "unit": "GFlop/s", "note": "host-buffer e2e is measured at N=1",
                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
@@ -333,6 +351,7 @@ def main():
                          "frac_of_probe_max": round(achieved / max(probe_copy, probe_read), 4),
                          "algorithmic_bytes_per_step": b_min},
             "e2e": e2e,
+            "perf_model": model,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -263,8 +263,8 @@ int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gb
 /* Tuning knob (process-wide): pJDS kernel variant with `rows_per_thread` R in {1,2,4} consecutive
    sorted rows per thread (vector loads, R independent FMA chains) and j-unroll `unroll` in {2,4,8}.
    (0, 0) restores the automatic choice.  R is reduced until it divides block_rows.  Every
-   variant computes bit-identical y (one FMA chain per row, stored order).  unroll + 16 also
-   enables a tile-wide L2 bulk prefetch of val/col (measured slower; kept for A/B runs);
+   variant computes bit-identical y (one FMA chain per row, stored order).  unroll + 16 selects
+   the software-pipelined main loop (next chunk's loads issued before the current FMAs);
    rows_per_thread + 8 forces the 64-bit jagged-offset kernels (used when stored + n_pad >= 2^31)
    on any matrix, so tests can cover them. */
 int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);

@@ -141,19 +141,14 @@ constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
 enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 3 };
 
 // ---- pJDS kernel -----------------------------------------------------------------------------
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
-               : "memory");
-}
 
 // Thread t owns the R consecutive sorted rows k0 = R*t .. R*t+R-1 (R divides b_r, so they share
 // one pJDS block and its length).  A warp covers 32R rows = one or several consecutive blocks;
 // lanes of a block loop to that block's length (PAPER.md L219-222 / Listing 2, reading 6).
-// PF: before computing, lane 0 of each warp issues one L2 bulk prefetch (UBLKPF) per jagged
-// column for the warp's contiguous val/col segment, so the HBM stream of the whole warp tile is
-// in flight at once, independent of registers; the loads below then hit L2.
+// PIPE: software-pipelined main loop (next chunk's val/col loads in flight during the current
+// chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
-template <typename T, typename Off, int R, int U, int MODE, bool PF>
+template <typename T, typename Off, int R, int U, int MODE, bool PIPE>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
@@ -181,20 +176,49 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const uint64_t pol_s = make_policy(pol & 0xff);
   const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
   auto cs = [&](int j) -> Off { return j < kSmemCS ? s_cs[j] : (Off)col_start[j]; };
-  if (PF) {
-    if ((threadIdx.x & 31) == 0) {
-      for (int j = 0; j < wlen; ++j) {
-        const Off o = cs(j) + (Off)warp_k0;
-        const Off e = min(o + (Off)(32 * R), cs(j + 1));  // stay inside jagged column j
-        if (e > o) {
-          prefetch_l2(val + o, (uint32_t)((e - o) * sizeof(T)), pol_s);
-          prefetch_l2(col + o, (uint32_t)((e - o) * 4), pol_s);
+  int j = 0;
+  if (PIPE && U <= len) {
+    // software pipeline: the val/col loads of chunk j+U are issued before the FMAs of chunk j, so
+    // the stream of the next chunk overlaps the dependent x gathers of the current one
+    Vec<T, R> va[U];
+    Vec<int, R> ca[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const Off o = cs(u) + (Off)k0;
+      va[u].load(val + o, pol_s);
+      ca[u].load(col + o, pol_s);
+    }
+    for (;;) {
+      T xv[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) xv[u][r] = ld_rhs(x + ca[u].v[r], pol_x);
+      const int jn = j + U;
+      const bool more = jn + U <= len;
+      Vec<T, R> vb[U];
+      Vec<int, R> cb[U];
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const Off o = cs(jn + u) + (Off)k0;
+          vb[u].load(val + o, pol_s);
+          cb[u].load(col + o, pol_s);
         }
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma_rn(va[u].v[r], xv[u][r], acc[r]);
+      j = jn;
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        va[u] = vb[u];
+        ca[u] = cb[u];
+      }
     }
-    __syncwarp();
   }
-  int j = 0;
   for (; j + U <= len; j += U) {  // full chunks: no predicates, all U loads issued back to back
     Vec<T, R> v[U];
     Vec<int, R> c[U];
@@ -298,7 +322,7 @@ int set_tile_order_impl(int mode) {
   g_tile_order = mode;
   return PJDS_OK;
 }
-static bool g_prefetch = false;  // measured: the tile-wide L2 bulk prefetch slows every config
+static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
 
 template <typename T, typename Off, int R, int U>
 int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part, int64_t* nparts) {
@@ -318,7 +342,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part)
 #define PJDS_LAUNCH(M)             \
-  if (g_prefetch) PJDS_LAUNCH_PF(M, true); \
+  if (g_pipe) PJDS_LAUNCH_PF(M, true); \
   else PJDS_LAUNCH_PF(M, false)
   if (mode == STORE_DIRECT) {
     PJDS_LAUNCH(STORE_DIRECT);
@@ -476,7 +500,7 @@ int set_cache_policy(int stream_kind, int x_kind) {
 }
 
 int set_kernel_variant(int r, int u) {
-  // u >= 16 encodes "with the tile-wide L2 bulk prefetch" (u - 16) for A/B measurements
+  // u >= 16 encodes "software-pipelined main loop" (u - 16)
   const bool pf = u >= 16;
   if (u >= 16) u -= 16;
   const bool off64 = r >= 8;  // rows_per_thread + 8: force 64-bit jagged offsets
@@ -485,7 +509,7 @@ int set_kernel_variant(int r, int u) {
     return set_error(PJDS_ERR_INVALID_ARG, "variant: rows_per_thread in {1,2,4}, unroll in {2,4,8} (or 0,0)");
   g_var_r = r;
   g_var_u = u;
-  g_prefetch = pf;
+  g_pipe = pf;
   g_force_off64 = off64;
   return PJDS_OK;
 }

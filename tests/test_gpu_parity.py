@@ -50,7 +50,7 @@ SMALL = [("uniform", 1000, {}), ("clustered", 777, {}), ("empty_rows", 513, {}),
 
 @pytest.mark.parametrize("kind,n,kw", SMALL)
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("br", [32, 64, 128])
+@pytest.mark.parametrize("br", [32, 64, 96, 128, 160])
 def test_pjds_small(pj, kind, n, kw, dtype, br):
     _, rp, col, val = inputs.small(kind, n, seed=br + n, dtype=dtype, **kw)
     x = inputs.vector(n, dtype)

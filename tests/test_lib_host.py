@@ -49,7 +49,7 @@ def assert_pjds_equal(got, P):
 
 
 @pytest.mark.parametrize("kind,n,kw", CASES)
-@pytest.mark.parametrize("br", [32, 64, 128])
+@pytest.mark.parametrize("br", [32, 64, 96, 128, 160])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_pjds_conversion_bit_exact(pj, kind, n, kw, br, dtype):
     _, rp, col, val = inputs.small(kind, n, seed=br, dtype=dtype, **kw)
