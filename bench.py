@@ -42,6 +42,8 @@ CONFIG_DESC = {
     "C3": "HMEp Holstein-Hubbard M=15, N=6201600",
     "C4": "DLR1-shaped 46417 points x 6, N=278502",
     "C5": "HMEp Holstein-Hubbard M=25 nested spin-grid, N=57002400",
+    "W4": "DLR2-shaped 108396 points x 5 (dense 5x5 blocks), N=541980, N_nzr~314",
+    "W5": "UHBR-shaped 900000 points x 5, N=4500000, N_nzr~122",
 }
 METRIC = "pJDS DP spMVM GFlop/s & HBM GB/s (% roofline) at 1/2/4/8 B200; bytes vs ELLPACK-R"
 # electronic-block size P (rows per contiguous off-diagonal segment) for partitioning

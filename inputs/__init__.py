@@ -47,7 +47,7 @@ def _load():
     return _lib
 
 
-HMEP, HMEP_BANDED, SAMG, DLR1 = 0, 1, 2, 3
+HMEP, HMEP_BANDED, SAMG, DLR1, DLR2, UHBR = 0, 1, 2, 3, 4, 5
 
 
 @dataclass(frozen=True)
@@ -66,6 +66,9 @@ CONFIGS = {
     "C3": Config("C3", HMEP, 15, 0, desc="HMEp physical M=15, N=6,201,600"),
     "C4": Config("C4", DLR1, desc="DLR1-shaped, N=278,502"),
     "C5": Config("C5", HMEP, 25, 1, desc="HMEp physical M=25 nested spin-grid, N=57,002,400"),
+    # NEXT-4 workloads: long rows, dense 5x5 blocks
+    "W4": Config("W4", DLR2, desc="DLR2-shaped 108,396 points x 5, N=541,980, N_nzr~315 (PAPER.md L121-127)"),
+    "W5": Config("W5", UHBR, desc="UHBR-shaped 900,000 points x 5, N=4,500,000, N_nzr~123 (PAPER.md L129-138)"),
 }
 
 

@@ -48,7 +48,7 @@ inline double unit_pm1(uint64_t h) {  // [-1, 1), 53-bit resolution
 }
 inline double unit01(uint64_t h) { return (double)(h >> 11) * (1.0 / 9007199254740992.0); }
 
-enum Family { HMEP = 0, HMEP_BANDED = 1, SAMG = 2, DLR1 = 3 };
+enum Family { HMEP = 0, HMEP_BANDED = 1, SAMG = 2, DLR1 = 3, DLR2 = 4, UHBR = 5 };
 
 struct Gen {
   int family = 0;
@@ -64,6 +64,7 @@ struct Gen {
   std::vector<int32_t> pt_of_row, row_of_pt;        // Morton order
   // DLR1
   std::vector<int32_t> nb_ptr, nb;                  // per point: sorted neighbour point ids (incl. self)
+  int bs = 6;                                       // unknowns per point
   virtual ~Gen() {}
 };
 
@@ -269,8 +270,11 @@ int samg_row(const Gen& g, int64_t r, int32_t* cols) {
 }
 
 // ---------------------------------------------------------------- DLR1-shaped (C4)
-void build_dlr1(Gen& g) {
-  const int G = 36, NDROP = 239;
+// Block k-NN family: G^3 jittered grid points minus NDROP hash-chosen ones, Morton-ordered, B
+// unknowns per point (dense B x B coupling blocks) to the d_p - 1 nearest points within a +-W cell
+// window.  kind 0 = DLR1 pmf, 1 = DLR2 (d_p: 60 % uniform 28..60, 40 % uniform 61..121 -> N_nzr ~
+// 315, N^max 605, ELLPACK reduction ~ 48 % as Table 1), 2 = UHBR (d_p uniform 18..31, N_nzr ~ 123).
+void build_blockknn(Gen& g, int G, int NDROP, int B, int kind, int W) {
   const int NP = G * G * G;
   std::vector<uint64_t> hk(NP);
   for (int i = 0; i < NP; ++i) hk[i] = (hash3(g.seed, (uint64_t)i, 0xD409) & ~0xffffull) | 0;
@@ -309,7 +313,9 @@ void build_dlr1(Gen& g) {
   for (int i = 0; i < npts; ++i) {
     double u = unit01(hash3(g.seed, (uint64_t)grid_of_id[i], 0xDDDD));
     int d;
-    if (u < 0.2) d = 15 + std::min(8, (int)(u / (0.2 / 9)));
+    if (kind == 1) d = u < 0.6 ? 28 + std::min(32, (int)(u / 0.6 * 33)) : 61 + std::min(60, (int)((u - 0.6) / 0.4 * 61));
+    else if (kind == 2) d = 18 + std::min(13, (int)(u * 14));
+    else if (u < 0.2) d = 15 + std::min(8, (int)(u / (0.2 / 9)));
     else {
       double acc = 0.2;
       d = 29;
@@ -328,9 +334,9 @@ void build_dlr1(Gen& g) {
     int pt = grid_of_id[i];
     int x = pt % G, y = (pt / G) % G, z = pt / (G * G);
     std::vector<std::pair<double, int>> cand;
-    for (int dz = -3; dz <= 3; ++dz)
-      for (int dy = -3; dy <= 3; ++dy)
-        for (int dx = -3; dx <= 3; ++dx) {
+    for (int dz = -W; dz <= W; ++dz)
+      for (int dy = -W; dy <= W; ++dy)
+        for (int dx = -W; dx <= W; ++dx) {
           int a = x + dx, b = y + dy, c = z + dz;
           if (a < 0 || b < 0 || c < 0 || a >= G || b >= G || c >= G) continue;
           int j = id_of_grid[a + G * (b + G * c)];
@@ -349,13 +355,15 @@ void build_dlr1(Gen& g) {
     for (int j : lists[i]) g.nb.push_back(j);
     g.nb_ptr[i + 1] = (int32_t)g.nb.size();
   }
-  g.n = (int64_t)npts * 6;
+  g.bs = B;
+  g.n = (int64_t)npts * B;
 }
 int dlr1_row(const Gen& g, int64_t r, int32_t* cols) {
-  int i = (int)(r / 6);
+  const int B = g.bs;
+  int i = (int)(r / B);
   int k = 0;
   for (int h = g.nb_ptr[i]; h < g.nb_ptr[i + 1]; ++h)
-    for (int c = 0; c < 6; ++c) cols[k++] = (int32_t)(g.nb[h] * 6 + c);
+    for (int c = 0; c < B; ++c) cols[k++] = (int32_t)(g.nb[h] * B + c);
   return k;  // already ascending
 }
 
@@ -364,17 +372,20 @@ int row_cols(const Gen& g, int64_t r, int32_t* cols) {
     case HMEP: return hmep_row(g, r, cols);
     case HMEP_BANDED: return hmep_banded_row(g, r, cols);
     case SAMG: return samg_row(g, r, cols);
-    case DLR1: return dlr1_row(g, r, cols);
+    case DLR1:
+    case DLR2:
+    case UHBR: return dlr1_row(g, r, cols);
   }
   return 0;
 }
-const int kMaxRow = 256;
+const int kMaxRow = 1024;
 
 }  // namespace
 
 extern "C" {
 
-// family: 0 HMEP (p0 = M, p1 = ordering), 1 HMEP_BANDED, 2 SAMG (p0,p1,p2 = nx,ny,nz), 3 DLR1.
+// family: 0 HMEP (p0 = M, p1 = ordering), 1 HMEP_BANDED, 2 SAMG (p0,p1,p2 = nx,ny,nz), 3 DLR1,
+// 4 DLR2, 5 UHBR.
 // Returns nullptr on bad arguments.
 void* pjdsgen_create(int family, int p0, int p1, int p2, uint64_t seed) {
   Gen* g = new (std::nothrow) Gen();
@@ -391,7 +402,9 @@ void* pjdsgen_create(int family, int p0, int p1, int p2, uint64_t seed) {
       if (p0 < 2 || p1 < 2 || p2 < 2 || p0 > 1024 || p1 > 1024 || p2 > 1024) { delete g; return nullptr; }
       build_samg(*g, p0, p1, p2);
       break;
-    case DLR1: build_dlr1(*g); break;
+    case DLR1: build_blockknn(*g, 36, 239, 6, 0, 3); break;          // 46,417 points x 6
+    case DLR2: build_blockknn(*g, 48, 2196, 5, 1, 4); break;         // 108,396 points x 5
+    case UHBR: build_blockknn(*g, 97, 12673, 5, 2, 3); break;        // 900,000 points x 5
     default: delete g; return nullptr;
   }
   return g;
