@@ -222,6 +222,19 @@ class DistPlan:
             pass
 
 
+def _nccl_path():
+    """The libnccl.so.2 torch uses (the pip nvidia-nccl package), so libpjds and torch share one
+    NCCL; None lets the library fall back to the loader's search path."""
+    import glob
+    import os
+    import site
+    for d in site.getsitepackages():
+        hits = glob.glob(os.path.join(d, "nvidia", "nccl", "lib", "libnccl.so*"))
+        if hits:
+            return sorted(hits)[0].encode()
+    return None
+
+
 def exchange_lists(recv_counts, recv_cols, group=None):
     """Turn every rank's recv lists into its send lists with torch.distributed all_to_all_single
     (setup-time plumbing; works on gloo (CPU) and NCCL (CUDA tensors))."""
@@ -266,6 +279,7 @@ class DistPjds:
         sc, scols = exchange_lists(rc, rcols, group)
         uid = (ctypes.c_char * 128)()
         if R > 1:
+            call("pjds_nccl_load", _nccl_path())
             if rank == 0:
                 call("pjds_nccl_unique_id", uid)
             obj = [bytes(uid) if rank == 0 else None]
