@@ -133,6 +133,9 @@ template <> struct Vec<int, 4> {
 
 constexpr int kThreads = 256;
 constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
+#ifndef PJDS_MINB
+#define PJDS_MINB 1  // measured: capping registers for 6 CTAs/SM (<= 40 regs) is 3-15 % slower in DP
+#endif
 
 // Store modes: y[perm[k]] = acc (row-only basis), y[k] = acc (permuted basis, PJDS_PERM_SYMMETRIC),
 // y[perm[k]] += acc (dist nonlocal part: the result is written twice).
@@ -149,7 +152,7 @@ enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 
 // chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
 template <typename T, typename Off, int R, int U, int MODE, bool PIPE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, PJDS_MINB)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
