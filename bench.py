@@ -271,6 +271,31 @@ def main():
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
         dist.all_reduce(lt)
         launches = int(lt.item())
+    dist_info = None
+    if world > 1:
+        # vector mode (exchange, then compute) as the reference point for "communication hidden",
+        # and one traced call of each mode: per-phase device times, max over ranks
+        dist.barrier()
+        ms_no = timed(lambda: D.spmv(y, x, stream=stream, no_overlap=True), max(5, a.steps // 4))
+        tt = torch.tensor([ms_no], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_no = float(tt.item())
+        phases = {}
+        for mode, no in (("task", False), ("vector", True)):
+            dist.barrier()
+            D.spmv(y, x, stream=stream, no_overlap=no, trace=True)
+            ph = D.trace()
+            vec = torch.tensor([ph[k] for k in sorted(ph)], dtype=torch.float64, device=dev)
+            dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+            phases[mode] = {k: round(v, 4) for k, v in zip(sorted(ph), vec.tolist())}
+        tp = phases["task"]
+        comm = max(tp["exchange"], 1e-9)
+        dist_info = {"ms_vector_mode": round(ms_no, 4), "speedup_task_over_vector": round(ms_no / ms, 3),
+                     "phases_ms_max_over_ranks": phases,
+                     "hidden_fraction": round(1.0 - max(0.0, tp["total"] - tp["local"] - tp["nonlocal"]
+                                                        - tp["pack"]) / comm, 3),
+                     "halo_entries_rank0": D.info["halo"], "nnz_nonlocal_rank0": D.info["nnz_nonlocal_part"],
+                     "messages_rank0": D.info["send_messages"]}
     t_s = ms * 1e-3
     gflops = 2.0 * nnz / t_s / 1e9
     # algorithmic bytes (Eq. 1 at alpha = 1/N_nzr, write-only y): val+col once, x once, y once
@@ -384,6 +409,7 @@ def main():
             "cpu_baseline": cpu,
             "footprint": footprint,
             "compare": compare or None,
+            "dist": dist_info,
             "setup_s": round(t_setup, 2),
         }
         print(json.dumps(out), flush=True)

@@ -190,7 +190,10 @@ enum {
   PJDS_TRANSPORT_LOCAL = 1  /* all ranks' handles in this process (pjds_dist_group_spmv);
                                halo moved with device-to-device copies; test harness */
 };
-enum { PJDS_NO_OVERLAP = 1u /* serialise exchange and compute (vector mode) */ };
+enum {
+  PJDS_NO_OVERLAP = 1u, /* serialise exchange and compute (vector mode) */
+  PJDS_TRACE = 2u       /* record phase events for pjds_dist_trace (Fig. 4 timeline analogue) */
+};
 
 /*
  * pjds_dist_create
@@ -223,6 +226,11 @@ typedef struct {
   int32_t permuted;
 } pjds_dist_info_t;
 int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* out);
+/* Phase timeline of the last pjds_dist_spmv call made with PJDS_TRACE (CUDA events on the compute
+   and comm streams; synchronises them): ms[0] total, [1] start -> local part done, [2] pack,
+   [3] NCCL exchange, [4] compute stream waiting for the exchange, [5] nonlocal part.
+   INVALID_ARG if no traced call was made. */
+int pjds_dist_trace(pjds_dist_t D, double* ms /* [6] */);
 /* The two pJDS parts (owned by D; do not destroy): A_loc, A_nl (A_nl may be NULL if empty). */
 int pjds_dist_parts(pjds_dist_t D, pjds_t* A_loc, pjds_t* A_nl);
 int pjds_dist_destroy(pjds_dist_t D);

@@ -334,11 +334,17 @@ class DistPjds:
         X = (ctypes.c_void_p * R)(*[_check_vec(x, h.n_loc, h.dtype, "x").value for x, h in zip(xs, handles)])
         call("pjds_dist_group_spmv", H, R, Y, X, _stream_ptr(stream), PJDS_NO_OVERLAP if no_overlap else 0)
 
-    def spmv(self, y_loc, x_loc, stream=None, no_overlap: bool = False):
+    def spmv(self, y_loc, x_loc, stream=None, no_overlap: bool = False, trace: bool = False):
         call("pjds_dist_spmv", self._h, _check_vec(y_loc, self.n_loc, self.dtype, "y"),
              _check_vec(x_loc, self.n_loc, self.dtype, "x"), _stream_ptr(stream),
-             PJDS_NO_OVERLAP if no_overlap else 0)
+             (PJDS_NO_OVERLAP if no_overlap else 0) | (_lib.PJDS_TRACE if trace else 0))
         return y_loc
+
+    def trace(self):
+        """Phase times (ms) of the last traced spmv: total, local, pack, exchange, wait, nonlocal."""
+        ms = np.zeros(6)
+        call("pjds_dist_trace", self._h, ms.ctypes.data)
+        return dict(zip(("total", "local", "pack", "exchange", "wait", "nonlocal"), ms.tolist()))
 
     def to_permuted(self, dst, src, stream=None):
         call("pjds_dist_permute", self._h, _check_vec(dst, self.n_loc, self.dtype, "dst"),

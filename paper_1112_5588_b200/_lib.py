@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(_HERE, "libpjds.so")
 PJDS_F32, PJDS_F64 = 0, 1
 PJDS_PERM_ROWS, PJDS_PERM_SYMMETRIC, PJDS_HOST_ONLY = 0, 1, 2
 PJDS_TRANSPORT_NCCL, PJDS_TRANSPORT_LOCAL = 0, 1
-PJDS_NO_OVERLAP = 1
+PJDS_NO_OVERLAP, PJDS_TRACE = 1, 2
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "BAD_CSR", -3: "OOM", -4: "CUDA", -5: "NCCL", -6: "UNSUPPORTED"}
 
 c_i64, c_i32, c_u32, c_p, c_dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_double
@@ -73,6 +73,7 @@ _SIGS = {
     "pjds_dist_spmv": [c_p, c_p, c_p, c_p, c_u32],
     "pjds_dist_group_spmv": [c_p, c_i32, c_p, c_p, c_p, c_u32],
     "pjds_dist_info": [c_p, c_p],
+    "pjds_dist_trace": [c_p, c_p],
     "pjds_dist_parts": [c_p, c_p, c_p],
     "pjds_dist_destroy": [c_p],
     "pjds_nccl_load": [ctypes.c_char_p],

@@ -135,6 +135,10 @@ struct pjds_dist {
   // streams / events
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
+  // phase timing (PJDS_TRACE): 0 start, 1 comm start, 2 pack end, 3 comm end, 4 local end,
+  // 5 nonlocal start (after the wait), 6 end
+  cudaEvent_t tev[7] = {};
+  bool traced = false;
   ncclComm_t nccl = nullptr;
   int send_messages = 0, recv_messages = 0;
   bool permuted = false;
@@ -436,6 +440,8 @@ int pjds_dist_destroy(pjds_dist_t D) {
   if (D->comm) cudaStreamDestroy(D->comm);
   if (D->ev_ready) cudaEventDestroy(D->ev_ready);
   if (D->ev_comm) cudaEventDestroy(D->ev_comm);
+  for (auto e : D->tev)
+    if (e) cudaEventDestroy(e);
   cudaFree(D->d_halo); cudaFree(D->d_packbuf); cudaFree(D->d_pack_idx);
   pjds_destroy(D->A_loc);
   pjds_destroy(D->A_nl);
@@ -473,26 +479,68 @@ int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t
   if (D->transport != PJDS_TRANSPORT_NCCL) return set_error(PJDS_ERR_INVALID_ARG, "use pjds_dist_group_spmv for LOCAL transport");
   cudaStream_t s = (cudaStream_t)stream;
   const bool comm_needed = D->R > 1 && (!D->sends.empty() || !D->recvs.empty());
+  const bool tr = flags & PJDS_TRACE;
+  if (tr && !D->tev[0])
+    for (auto& e : D->tev) PJDS_CUDA_TRY(cudaEventCreate(&e));
+  auto mark = [&](int i, cudaStream_t st) -> int {
+    if (tr) PJDS_CUDA_TRY(cudaEventRecord(D->tev[i], st));
+    return PJDS_OK;
+  };
   if (!comm_needed) {  // R = 1 or no halo: local part only (+ empty nonlocal)
+    for (int i = 0; i < 4; ++i) PJDS_TRY(mark(i, s));
     PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+    for (int i = 4; i < 7; ++i) PJDS_TRY(mark(i, s));
+    D->traced = D->traced || tr;
     return PJDS_OK;
   }
-  if (flags & PJDS_NO_OVERLAP) {
+  if (flags & PJDS_NO_OVERLAP) {  // vector mode: exchange, then both parts, one stream
+    PJDS_TRY(mark(0, s));
+    PJDS_TRY(mark(1, s));
     if (D->packed_total) PJDS_TRY(launch_pack(D->d_pack_idx, D->packed_total, x, D->d_packbuf, D->dtype, s));
+    PJDS_TRY(mark(2, s));
     PJDS_TRY(post_nccl(D, x, s));
+    PJDS_TRY(mark(3, s));
     PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+    PJDS_TRY(mark(4, s));
+    PJDS_TRY(mark(5, s));
     if (D->A_nl) PJDS_TRY(launch_pjds_spmv(D->A_nl, y, D->d_halo, s, true));
+    PJDS_TRY(mark(6, s));
+    D->traced = D->traced || tr;
     return PJDS_OK;
   }
   // task mode: comm stream starts after x is ready on the compute stream
+  PJDS_TRY(mark(0, s));
   PJDS_CUDA_TRY(cudaEventRecord(D->ev_ready, s));
   PJDS_CUDA_TRY(cudaStreamWaitEvent(D->comm, D->ev_ready, 0));
+  PJDS_TRY(mark(1, D->comm));
   if (D->packed_total) PJDS_TRY(launch_pack(D->d_pack_idx, D->packed_total, x, D->d_packbuf, D->dtype, D->comm));
+  PJDS_TRY(mark(2, D->comm));
   PJDS_TRY(post_nccl(D, x, D->comm));
+  PJDS_TRY(mark(3, D->comm));
   PJDS_CUDA_TRY(cudaEventRecord(D->ev_comm, D->comm));
   PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+  PJDS_TRY(mark(4, s));
   PJDS_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_comm, 0));
+  PJDS_TRY(mark(5, s));
   if (D->A_nl) PJDS_TRY(launch_pjds_spmv(D->A_nl, y, D->d_halo, s, true));
+  PJDS_TRY(mark(6, s));
+  D->traced = D->traced || tr;
+  return PJDS_OK;
+}
+
+int pjds_dist_trace(pjds_dist_t D, double* ms) {
+  if (!D || !ms) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_trace: NULL argument");
+  if (!D->traced) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_trace: no traced pjds_dist_spmv call yet");
+  PJDS_CUDA_TRY(cudaEventSynchronize(D->tev[6]));
+  PJDS_CUDA_TRY(cudaEventSynchronize(D->tev[3]));
+  float t[7];
+  for (int i = 1; i < 7; ++i) PJDS_CUDA_TRY(cudaEventElapsedTime(&t[i], D->tev[0], D->tev[i]));
+  ms[0] = t[6];          // total
+  ms[1] = t[4];          // start -> local part done
+  ms[2] = t[2] - t[1];   // pack
+  ms[3] = t[3] - t[2];   // NCCL exchange
+  ms[4] = t[5] - t[4];   // compute stream waiting for the exchange after the local part
+  ms[5] = t[6] - t[5];   // nonlocal part
   return PJDS_OK;
 }
 
