@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--no-compare", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
+    p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
     return p.parse_args()
 
 
@@ -173,14 +174,19 @@ def main():
     dev = torch.device("cuda", local_rank)
     tdt = torch.float64 if npdt == np.float64 else torch.float32
     dist = None
-    if world > 1:
+    use_dist = world > 1 or a.dist
+    if use_dist:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29611")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
 
     t_setup = time.perf_counter()
     g = inputs.Generator.from_config(a.config)
     n = g.n
-    if world > 1:
+    if use_dist:
         seg = SEGMENT.get(a.config, 32)
         nb = n // seg
         offs = np.array([(nb * r // world) * seg for r in range(world + 1)], np.int64)
@@ -194,7 +200,7 @@ def main():
     permuted = a.impl == "pjds" and a.basis == "permuted"
     compare = {}
     footprint = None
-    if world > 1:
+    if use_dist:
         D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=permuted)
         A = None
     else:
@@ -218,7 +224,7 @@ def main():
                "sample": f"whole {a.config} matrix ({nnz_loc} nnz), {reps} products, median; {tot:.1f} s of "
                          f"oracle_spmv_crs ({np.dtype(npdt).name}, OpenMP {cores} threads)"}
     nnz = nnz_loc
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
         dist.all_reduce(tt)
         nnz = int(tt.item())
@@ -226,7 +232,7 @@ def main():
     y = torch.empty(hi - lo, dtype=tdt, device=dev)
     if permuted:
         xp = torch.empty_like(x)
-        (D if world > 1 else A).to_permuted(xp, x)  # once, before the "iterative scheme"
+        (D if use_dist else A).to_permuted(xp, x)  # once, before the "iterative scheme"
         x = xp
     t_setup = time.perf_counter() - t_setup
 
@@ -236,7 +242,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        if world > 1:
+        if use_dist:
             D.spmv(y, x, stream=stream, no_overlap=a.no_overlap)
         else:
             A.spmv(y, x, stream=stream)
@@ -254,17 +260,17 @@ def main():
     for _ in range(max(a.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = pj.launch_count()
     with ClockSampler(local_rank) as clk:
         ms = timed(step, a.steps)
     launches = pj.launch_count() - launches0
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
@@ -272,7 +278,7 @@ def main():
         dist.all_reduce(lt)
         launches = int(lt.item())
     dist_info = None
-    if world > 1:
+    if use_dist:
         # vector mode (exchange, then compute) as the reference point for "communication hidden",
         # and one traced call of each mode: per-phase device times, max over ranks
         dist.barrier()
@@ -304,7 +310,7 @@ def main():
     peak = peak_file if peak_file else max(probe_copy, probe_read)
 
     # side-by-side kernels on the same matrix (N=1): rows-only pJDS and ELLPACK-R
-    if world == 1 and a.impl == "pjds" and not a.no_compare:
+    if not use_dist and a.impl == "pjds" and not a.no_compare:
         x0 = torch.from_numpy(x_host).to(dev)
         for name, mk in (("pjds_rows_only" if permuted else "pjds_permuted",
                           lambda: pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows,
@@ -326,7 +332,7 @@ def main():
     # change, kernel, basis change back, D2H y, every step)
     e2e = None
     model = None
-    if world == 1 and a.impl == "pjds":
+    if not use_dist and a.impl == "pjds":
         xh = torch.from_numpy(x_host).pin_memory().numpy()
         yh = torch.empty(n, dtype=tdt).pin_memory().numpy()
         A.spmv_host(yh, xh)
@@ -349,7 +355,7 @@ def main():
                  "eq4_nnzr_lower_10pct_penalty": round(perfmodel.n_nzr_lower(ratio, alpha or perfmodel.RECIPROCAL), 1),
                  "n_nzr": round(nnz / n, 2),
                  "pci_share_of_e2e": round(t_pci_meas / te, 3)}
-    elif world > 1:
+    elif use_dist:
         # per rank: pinned host x_loc -> device, basis change, dist product, basis change back,
         # device -> pinned host y_loc, every step; max over ranks
         xh = torch.from_numpy(x_host).pin_memory()
@@ -390,13 +396,13 @@ def main():
             "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
             "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows,
                        "parallelism": f"row-partition r{world}" if world > 1 else "single GPU",
-                       "overlap": (not a.no_overlap) if world > 1 else None,
+                       "overlap": (not a.no_overlap) if use_dist else None,
                        "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
             "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": (committed_traffic(f"{a.config}/{a.dtype}/{a.basis}")
-                                     if world == 1 and a.impl == "pjds" else None),
+                                     if not use_dist and a.impl == "pjds" else None),
                          "traffic_source": "profiles/r01_traffic.json (ncu --set full, per launch)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peak_file else "bw probe (this run)",
                          "probe_copy_gbs": round(probe_copy, 1), "probe_read_gbs": round(probe_read, 1),
@@ -413,7 +419,7 @@ def main():
             "setup_s": round(t_setup, 2),
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         D.close()
         dist.destroy_process_group()

@@ -46,5 +46,6 @@ def test_dist_world1(pg, permuted):
         assert oracle.acceptance(yh, y_ref, bound, np.diff(rp), np.float64).all()
         assert np.array_equal(yh, oracle.spmv_chain(n, rp, col, val, x))
         ph = D.trace()
-        assert ph["total"] > 0 and ph["exchange"] == 0.0 and ph["nonlocal"] >= 0.0
+        # one rank: no exchange (back-to-back events only), the local part is the whole product
+        assert ph["total"] > 0 and ph["exchange"] < 0.05 and ph["local"] <= ph["total"] + 1e-6
     D.close()
