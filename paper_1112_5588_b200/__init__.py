@@ -228,6 +228,8 @@ def _nccl_path():
     import glob
     import os
     import site
+    if os.environ.get("PJDS_NCCL_LIB"):  # explicit choice (tests substitute a one-GPU stand-in)
+        return os.environ["PJDS_NCCL_LIB"].encode()
     for d in site.getsitepackages():
         hits = glob.glob(os.path.join(d, "nvidia", "nccl", "lib", "libnccl.so*"))
         if hits:

@@ -1,0 +1,44 @@
+"""Probe: can two NCCL ranks share one GPU here?  If yes, run the real NCCL dist path (R=2) on C1
+and compare with the oracle (dev tool)."""
+import os, sys, json
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
+import torch, torch.distributed as dist
+import inputs, oracle, paper_1112_5588_b200 as pj
+from oracle import dist as odist
+rank = int(os.environ["RANK"]); R = int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(0)
+dist.init_process_group("gloo")
+name = sys.argv[1] if len(sys.argv) > 1 else "C1"
+n, rp, col, val = inputs.config_crs(name)
+seg = {"C1": 1024, "C3": 15504}[name]
+nb = n // seg
+offs = np.array([(nb * r // R) * seg for r in range(R + 1)], np.int64)
+lo, hi = offs[rank], offs[rank + 1]
+x = inputs.vector(n)
+out = {}
+for permuted in (False, True):
+    try:
+        D = pj.DistPjds.create(n, offs, rp[lo:hi + 1] - rp[lo], col[rp[lo]:rp[hi]], val[rp[lo]:rp[hi]], permuted=permuted)
+    except Exception as e:
+        print(json.dumps({"rank": rank, "create_error": str(e)[:300]})); sys.exit(0)
+    xt = torch.from_numpy(x[lo:hi].copy()).cuda()
+    if permuted:
+        xt = D.to_permuted(torch.empty_like(xt), xt)
+    for no in (False, True):
+        y = torch.full_like(xt, float("nan"))
+        D.spmv(y, xt, no_overlap=no, trace=True)
+        if permuted:
+            y = D.from_permuted(torch.empty_like(y), y)
+        torch.cuda.synchronize()
+        ys = [None] * R
+        dist.all_gather_object(ys, y.cpu().numpy())
+        yall = np.concatenate(ys)
+        ref = odist.spmv(odist.split(n, rp, col, val, offs), x) if name == "C1" else None
+        yl, b = oracle.spmv_ld(n, rp, col, val, x)
+        ok = bool(oracle.acceptance(yall, yl, b, np.diff(rp), np.float64).all())
+        out[f"perm{int(permuted)}_noov{int(no)}"] = {"o2": ok, "bitwise_vs_split_oracle": bool(np.array_equal(yall, ref)) if ref is not None else None,
+                                                     "trace": D.trace(), "halo": D.info["halo"], "messages": D.info["send_messages"]}
+    D.close()
+print(json.dumps({"rank": rank, **out}))
+dist.destroy_process_group()
