@@ -1,8 +1,8 @@
-"""Probe: can two NCCL ranks share one GPU here?  If yes, run the real NCCL dist path (R=2) on C1
-and compare with the oracle (dev tool)."""
+"""Worker for tests/test_gpu_fake_nccl.py: one rank of the NCCL-transport dist path (all ranks on
+cuda:0; PJDS_NCCL_LIB selects the one-GPU NCCL stand-in).  Prints one JSON line per rank."""
 import os, sys, json
 import numpy as np
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, ROOT)
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, ROOT)
 import torch, torch.distributed as dist
 import inputs, oracle, paper_1112_5588_b200 as pj
 from oracle import dist as odist
@@ -10,8 +10,11 @@ rank = int(os.environ["RANK"]); R = int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(0)
 dist.init_process_group("gloo")
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
-n, rp, col, val = inputs.config_crs(name)
-seg = {"C1": 1024, "C3": 15504}[name]
+if name == "rand":
+    n, rp, col, val = inputs.small("random", 3000, seed=3, max=60)
+else:
+    n, rp, col, val = inputs.config_crs(name)
+seg = {"C1": 1024, "C3": 15504, "rand": 1}[name]
 nb = n // seg
 offs = np.array([(nb * r // R) * seg for r in range(R + 1)], np.int64)
 lo, hi = offs[rank], offs[rank + 1]
@@ -34,7 +37,7 @@ for permuted in (False, True):
         ys = [None] * R
         dist.all_gather_object(ys, y.cpu().numpy())
         yall = np.concatenate(ys)
-        ref = odist.spmv(odist.split(n, rp, col, val, offs), x) if name == "C1" else None
+        ref = odist.spmv(odist.split(n, rp, col, val, offs), x) if name != "C3" else None
         yl, b = oracle.spmv_ld(n, rp, col, val, x)
         ok = bool(oracle.acceptance(yall, yl, b, np.diff(rp), np.float64).all())
         out[f"perm{int(permuted)}_noov{int(no)}"] = {"o2": ok, "bitwise_vs_split_oracle": bool(np.array_equal(yall, ref)) if ref is not None else None,
