@@ -135,6 +135,17 @@ def measured_peaks():
         return {}
 
 
+def _allreduce(dist, t, op):
+    """all_reduce of a small CUDA tensor on either backend (gloo reduces host copies)."""
+    o = dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM
+    if dist.get_backend() == "gloo":
+        c = t.cpu()
+        dist.all_reduce(c, op=o)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=o)
+
+
 # ------------------------------------------------------------------------------------------ CPU oracle
 def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1):
     """The oracle's plain CRS loop (oracle_spmv_crs: OpenMP static over rows, all visible cores),
@@ -170,8 +181,10 @@ def main():
     import paper_1112_5588_b200 as pj
     from paper_1112_5588_b200 import perfmodel
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ngpu = torch.cuda.device_count()
+    dev_index = local_rank % max(ngpu, 1)  # more ranks than GPUs only in the one-GPU transport test
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     tdt = torch.float64 if npdt == np.float64 else torch.float32
     dist = None
     use_dist = world > 1 or a.dist
@@ -181,7 +194,10 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29611")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=dev)
+        if world <= ngpu:
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # oversubscribed (test of the transport on one GPU): NCCL refuses duplicate GPUs
+            dist.init_process_group("gloo")
 
     t_setup = time.perf_counter()
     g = inputs.Generator.from_config(a.config)
@@ -226,7 +242,7 @@ def main():
     nnz = nnz_loc
     if use_dist:
         tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
-        dist.all_reduce(tt)
+        _allreduce(dist, tt, "sum")
         nnz = int(tt.item())
     x = torch.from_numpy(x_host).to(dev)
     y = torch.empty(hi - lo, dtype=tdt, device=dev)
@@ -264,7 +280,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = pj.launch_count()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         ms = timed(step, a.steps)
     launches = pj.launch_count() - launches0
     if use_dist:
@@ -272,10 +288,10 @@ def main():
     torch.cuda.synchronize()
     if use_dist:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        _allreduce(dist, tt, "max")
         ms = float(tt.item())
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
-        dist.all_reduce(lt)
+        _allreduce(dist, lt, "sum")
         launches = int(lt.item())
     dist_info = None
     if use_dist:
@@ -284,7 +300,7 @@ def main():
         dist.barrier()
         ms_no = timed(lambda: D.spmv(y, x, stream=stream, no_overlap=True), max(5, a.steps // 4))
         tt = torch.tensor([ms_no], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        _allreduce(dist, tt, "max")
         ms_no = float(tt.item())
         phases = {}
         for mode, no in (("task", False), ("vector", True)):
@@ -292,7 +308,7 @@ def main():
             D.spmv(y, x, stream=stream, no_overlap=no, trace=True)
             ph = D.trace()
             vec = torch.tensor([ph[k] for k in sorted(ph)], dtype=torch.float64, device=dev)
-            dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+            _allreduce(dist, vec, "max")
             phases[mode] = {k: round(v, 4) for k, v in zip(sorted(ph), vec.tolist())}
         tp = phases["task"]
         comm = max(tp["exchange"], 1e-9)
@@ -378,7 +394,7 @@ def main():
         dist.barrier()
         te = timed(e2e_step, a.e2e_steps) * 1e-3
         tt = torch.tensor([te], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        _allreduce(dist, tt, "max")
         te = float(tt.item())
         e2e = {"value": round(2.0 * nnz / te / 1e9, 2), "unit": "GFlop/s", "h2d_bytes_per_step": n * sv,
                "d2h_bytes_per_step": n * sv, "ms_per_step": round(te * 1e3, 3),
