@@ -66,6 +66,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
+    p.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                   help="dist halo exchange: NCCL send/recv on a side stream, or the fused gather+put P2P kernel")
     return p.parse_args()
 
 
@@ -217,7 +219,8 @@ def main():
     compare = {}
     footprint = None
     if use_dist:
-        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=permuted)
+        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=permuted,
+                               transport=a.transport)
         A = None
     else:
         if a.impl == "ellr":
@@ -413,6 +416,7 @@ def main():
             "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows,
                        "parallelism": f"row-partition r{world}" if world > 1 else "single GPU",
                        "overlap": (not a.no_overlap) if use_dist else None,
+                       "transport": a.transport if use_dist else None,
                        "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
             "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -187,8 +187,13 @@ int pjds_dist_plan_destroy(pjds_plan_t P);
 
 enum {
   PJDS_TRANSPORT_NCCL = 0,  /* one process per GPU; nccl_unique_id = 128-byte ncclUniqueId */
-  PJDS_TRANSPORT_LOCAL = 1  /* all ranks' handles in this process (pjds_dist_group_spmv);
+  PJDS_TRANSPORT_LOCAL = 1, /* all ranks' handles in this process (pjds_dist_group_spmv);
                                halo moved with device-to-device copies; test harness */
+  PJDS_TRANSPORT_P2P = 2    /* one process per GPU (or several per GPU), no NCCL per call: a fused
+                               gather+put kernel stores the send entries straight into the
+                               receivers' halo buffers through CUDA-IPC mappings (NVLink P2P),
+                               release/acquire flags order put -> nonlocal part -> buffer reuse.
+                               Connect with pjds_dist_p2p_export / _connect after create. */
 };
 enum {
   PJDS_NO_OVERLAP = 1u, /* serialise exchange and compute (vector mode) */
@@ -212,6 +217,15 @@ enum {
 int pjds_dist_create(pjds_dist_t* out, pjds_plan_t plan, const void* val_loc, int dtype,
                      int32_t block_rows, const int64_t* send_counts, const int32_t* send_cols,
                      int32_t transport, const void* nccl_unique_id, uint32_t flags);
+/* PJDS_TRANSPORT_P2P setup (collective; the caller all-gathers the blobs, e.g. with
+   torch.distributed.all_gather_object):
+   pjds_dist_p2p_export: writes this rank's fixed-size blob (CUDA IPC handle of its halo/flag region
+     and its halo layout) to `blob` (may be NULL to query) and its size to *bytes.
+   pjds_dist_p2p_connect: `blobs` = nranks blobs in rank order; opens the peers' regions.
+   pjds_dist_p2p_check: *timed_out = 1 if a flag wait gave up (~10 s) since create (synchronous). */
+int pjds_dist_p2p_export(pjds_dist_t D, void* blob, int64_t* bytes);
+int pjds_dist_p2p_connect(pjds_dist_t D, const void* blobs, int64_t blob_bytes);
+int pjds_dist_p2p_check(pjds_dist_t D, int32_t* timed_out);
 /* Basis change of a local vector for PJDS_PERM_SYMMETRIC dist handles (see pjds_permute). */
 int pjds_dist_permute(pjds_dist_t D, void* dst, const void* src, int32_t direction, void* stream);
 /* y_loc = A[rows of this rank, :] x ; x_loc / y_loc device pointers of length n_loc. */

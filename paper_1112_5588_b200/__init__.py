@@ -270,9 +270,11 @@ class DistPjds:
 
     @classmethod
     def create(cls, n_global, offsets, rowptr_loc, col_loc, val_loc, block_rows: int = 32, group=None,
-               permuted: bool = False):
+               permuted: bool = False, transport: str = "nccl"):
         """Collective over the torch.distributed default (or given) group: one rank per GPU.
-        permuted: x_loc / y_loc live in the local permuted basis (to_permuted / from_permuted)."""
+        permuted: x_loc / y_loc live in the local permuted basis (to_permuted / from_permuted).
+        transport: "nccl" (grouped send/recv on a side stream) or "p2p" (fused gather+put kernel
+        into the peers' halo buffers through CUDA-IPC mappings, no NCCL per call)."""
         import torch.distributed as dist
         R, rank = dist.get_world_size(group), dist.get_rank(group)
         val_loc = np.ascontiguousarray(val_loc)
@@ -280,7 +282,8 @@ class DistPjds:
         rc, rcols = plan.recv()
         sc, scols = exchange_lists(rc, rcols, group)
         uid = (ctypes.c_char * 128)()
-        if R > 1:
+        tr = {"nccl": PJDS_TRANSPORT_NCCL, "p2p": _lib.PJDS_TRANSPORT_P2P}[transport]
+        if R > 1 and transport == "nccl":
             call("pjds_nccl_load", _nccl_path())
             if rank == 0:
                 call("pjds_nccl_unique_id", uid)
@@ -289,10 +292,25 @@ class DistPjds:
             ctypes.memmove(uid, obj[0], 128)
         h = ctypes.c_void_p()
         call("pjds_dist_create", ctypes.byref(h), plan._h, val_loc.ctypes.data, _dt(val_loc), int(block_rows),
-             sc.ctypes.data, scols.ctypes.data, PJDS_TRANSPORT_NCCL, uid, PJDS_PERM_SYMMETRIC if permuted else 0)
+             sc.ctypes.data, scols.ctypes.data, tr, uid, PJDS_PERM_SYMMETRIC if permuted else 0)
+        if transport == "p2p":
+            nb = ctypes.c_int64()
+            call("pjds_dist_p2p_export", h, None, ctypes.byref(nb))
+            blob = (ctypes.c_char * nb.value)()
+            call("pjds_dist_p2p_export", h, blob, ctypes.byref(nb))
+            blobs = [None] * R
+            dist.all_gather_object(blobs, bytes(blob), group=group)
+            allb = b"".join(blobs)
+            call("pjds_dist_p2p_connect", h, ctypes.c_char_p(allb), nb.value)
+            dist.barrier(group=group)
         info = plan.info
         plan.close()
         return cls(h, info, R, rank, _dt(val_loc))
+
+    def p2p_timed_out(self) -> bool:
+        v = ctypes.c_int32()
+        call("pjds_dist_p2p_check", self._h, ctypes.byref(v))
+        return bool(v.value)
 
     @classmethod
     def create_group(cls, n, rowptr, col, val, offsets, block_rows: int = 32, permuted: bool = False):

@@ -142,6 +142,25 @@ struct pjds_dist {
   ncclComm_t nccl = nullptr;
   int send_messages = 0, recv_messages = 0;
   bool permuted = false;
+  // ---- P2P transport (p2p.cu): IPC-exported region [halo0 | halo1 | ready[R] | done[R] | err]
+  char* p2p_region = nullptr;
+  size_t p2p_halo_bytes = 0, p2p_region_bytes = 0;
+  std::vector<int64_t> recv_off;               // my halo offset (entries) of each owner's segment
+  std::vector<int32_t> send_peers, recv_peers;  // peers I send to / receive from (ascending rank)
+  int32_t* d_p2p_idx = nullptr;                 // send ids of all send peers, concatenated
+  int64_t* d_p2p_seg = nullptr;                 // [send_peers+1] segment starts
+  int64_t p2p_max_count = 0;
+  int32_t* d_send_peers = nullptr;              // for the done-wait
+  int32_t* d_recv_peers = nullptr;              // for the ready-wait
+  void** d_dst[2] = {nullptr, nullptr};         // per buffer parity: destination pointer per send peer
+  uint64_t** d_ready_targets = nullptr;         // ready[rank] slot in each receiver's region
+  uint64_t** d_done_targets = nullptr;          // done[rank] slot in each sender's region
+  std::vector<void*> peer_regions;              // opened IPC mappings
+  bool p2p_connected = false;
+  uint64_t seq = 0;
+  uint64_t* ready_flags() const { return (uint64_t*)(p2p_region + 2 * p2p_halo_bytes); }
+  uint64_t* done_flags() const { return ready_flags() + R; }
+  unsigned* err_flag() const { return (unsigned*)(done_flags() + R); }
 };
 
 namespace {
@@ -163,6 +182,38 @@ int post_nccl(pjds_dist* D, const void* x_loc, cudaStream_t s) {
   NCCL_TRY(g_nccl.groupEnd());
   return PJDS_OK;
 }
+
+// P2P transport: allocate the IPC-exported region and the per-call device tables.
+int p2p_setup(pjds_dist* D, const std::vector<int32_t>& ids, const std::vector<int64_t>& seg) {
+  const size_t vs = vsz(D);
+  D->p2p_halo_bytes = (std::max<size_t>(D->halo * vs, 16) + 255) / 256 * 256;
+  D->p2p_region_bytes = 2 * D->p2p_halo_bytes + 2 * (size_t)D->R * 8 + 256;
+  PJDS_CUDA_TRY(cudaMalloc(&D->p2p_region, D->p2p_region_bytes));
+  PJDS_CUDA_TRY(cudaMemset(D->p2p_region, 0, D->p2p_region_bytes));
+  const size_t ns = D->send_peers.size(), nr = D->recv_peers.size();
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_p2p_idx, std::max<size_t>(ids.size(), 1) * 4));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_p2p_seg, seg.size() * 8));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_send_peers, std::max<size_t>(ns, 1) * 4));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_recv_peers, std::max<size_t>(nr, 1) * 4));
+  for (auto& d : D->d_dst) PJDS_CUDA_TRY(cudaMalloc(&d, std::max<size_t>(ns, 1) * sizeof(void*)));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_ready_targets, std::max<size_t>(ns, 1) * sizeof(void*)));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_done_targets, std::max<size_t>(nr, 1) * sizeof(void*)));
+  if (!ids.empty()) PJDS_CUDA_TRY(cudaMemcpy(D->d_p2p_idx, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice));
+  PJDS_CUDA_TRY(cudaMemcpy(D->d_p2p_seg, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice));
+  if (ns) PJDS_CUDA_TRY(cudaMemcpy(D->d_send_peers, D->send_peers.data(), ns * 4, cudaMemcpyHostToDevice));
+  if (nr) PJDS_CUDA_TRY(cudaMemcpy(D->d_recv_peers, D->recv_peers.data(), nr * 4, cudaMemcpyHostToDevice));
+  D->peer_regions.assign(D->R, nullptr);
+  return PJDS_OK;
+}
+
+// Fixed-size blob each rank publishes: IPC handle of its region plus its halo layout.
+constexpr int kP2PMaxRanks = 64;
+struct P2PBlob {
+  cudaIpcMemHandle_t handle;
+  uint64_t halo_bytes;
+  int32_t R, rank;
+  int64_t recv_off[kP2PMaxRanks];
+};
 
 }  // namespace
 
@@ -295,7 +346,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
   if (flags & ~(uint32_t)PJDS_PERM_SYMMETRIC) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: unknown flags");
   const bool sym = flags & PJDS_PERM_SYMMETRIC;
   if (dtype != PJDS_F32 && dtype != PJDS_F64) return set_error(PJDS_ERR_INVALID_ARG, "bad dtype");
-  if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL)
+  if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL && transport != PJDS_TRANSPORT_P2P)
     return set_error(PJDS_ERR_INVALID_ARG, "bad transport");
   if (P->nnz_loc > 0 && !val) return set_error(PJDS_ERR_INVALID_ARG, "val is NULL");
   if (P->R > 1 && !send_counts) return set_error(PJDS_ERR_INVALID_ARG, "send_counts is NULL");
@@ -323,6 +374,8 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
   const size_t vs = dtype_size(dtype);
   int s = PJDS_OK;
   auto fail = [&](int st) { pjds_dist_destroy(D); return st; };
+  std::vector<int32_t> p2p_ids;
+  std::vector<int64_t> p2p_seg;
   try {
     // ---- the two pJDS parts
     std::vector<uint8_t> v_loc(P->loc_src.size() * vs), v_nl(P->nl_src.size() * vs);
@@ -359,6 +412,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
     D->permuted = sym;
     // ---- send schedule
     int64_t pos = 0;
+    p2p_seg.push_back(0);
     for (int q = 0; q < R && send_counts; ++q) {
       const int64_t cnt = send_counts[q];
       if (!cnt) continue;
@@ -367,6 +421,12 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       if (sym)
         for (auto& v : ids) v = inv[v];  // gather from x in the local permuted basis
       pos += cnt;
+      if (transport == PJDS_TRANSPORT_P2P) {  // every entry is gathered by the fused pack+put kernel
+        p2p_ids.insert(p2p_ids.end(), ids.begin(), ids.end());
+        p2p_seg.push_back((int64_t)p2p_ids.size());
+        D->send_peers.push_back(q);
+        D->p2p_max_count = std::max(D->p2p_max_count, cnt);
+      }
       auto runs = runs_of(ids.data(), cnt);
       pjds_dist::PeerSend ps;
       ps.peer = q;
@@ -384,9 +444,12 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
     }
     // ---- recv schedule (same run rule on the same lists)
     int64_t hoff = 0;
+    D->recv_off.assign(R, 0);
     for (int q = 0; q < R; ++q) {
+      D->recv_off[q] = hoff;
       const int64_t cnt = P->recv_counts[q];
       if (!cnt) continue;
+      D->recv_peers.push_back(q);
       auto runs = runs_of(P->recv_cols.data() + hoff, cnt);
       pjds_dist::PeerRecv pr;
       pr.peer = q;
@@ -407,9 +470,12 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
     return fail(set_error(PJDS_ERR_OOM, "host allocation failed in pjds_dist_create"));
   }
   // ---- device buffers, streams, transport
-  if (cudaMalloc(&D->d_halo, std::max<size_t>(D->halo * vs, 16)) != cudaSuccess)
+  if (transport == PJDS_TRANSPORT_P2P) {
+    if ((s = p2p_setup(D, p2p_ids, p2p_seg)) != PJDS_OK) return fail(s);
+  } else if (cudaMalloc(&D->d_halo, std::max<size_t>(D->halo * vs, 16)) != cudaSuccess) {
     return fail(set_error(PJDS_ERR_OOM, "halo allocation failed"));
-  if (D->packed_total) {
+  }
+  if (D->packed_total && transport != PJDS_TRANSPORT_P2P) {
     if (cudaMalloc(&D->d_packbuf, D->packed_total * vs) != cudaSuccess ||
         cudaMalloc(&D->d_pack_idx, D->packed_total * 4) != cudaSuccess)
       return fail(set_error(PJDS_ERR_OOM, "pack buffer allocation failed"));
@@ -443,9 +509,88 @@ int pjds_dist_destroy(pjds_dist_t D) {
   for (auto e : D->tev)
     if (e) cudaEventDestroy(e);
   cudaFree(D->d_halo); cudaFree(D->d_packbuf); cudaFree(D->d_pack_idx);
+  for (void* p : D->peer_regions)
+    if (p) cudaIpcCloseMemHandle(p);
+  cudaFree(D->p2p_region); cudaFree(D->d_p2p_idx); cudaFree(D->d_p2p_seg);
+  cudaFree(D->d_send_peers); cudaFree(D->d_recv_peers);
+  cudaFree(D->d_dst[0]); cudaFree(D->d_dst[1]); cudaFree(D->d_ready_targets); cudaFree(D->d_done_targets);
   pjds_destroy(D->A_loc);
   pjds_destroy(D->A_nl);
   delete D;
+  return PJDS_OK;
+}
+
+int pjds_dist_p2p_export(pjds_dist_t D, void* blob, int64_t* bytes) {
+  if (!D || !bytes) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_export: NULL argument");
+  if (D->transport != PJDS_TRANSPORT_P2P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_export: not a P2P handle");
+  if (D->R > kP2PMaxRanks) return set_error(PJDS_ERR_UNSUPPORTED, "P2P transport supports at most 64 ranks");
+  *bytes = (int64_t)sizeof(P2PBlob);
+  if (!blob) return PJDS_OK;
+  P2PBlob b;
+  std::memset(&b, 0, sizeof(b));
+  PJDS_CUDA_TRY(cudaIpcGetMemHandle(&b.handle, D->p2p_region));
+  b.halo_bytes = D->p2p_halo_bytes;
+  b.R = D->R;
+  b.rank = D->rank;
+  for (int q = 0; q < D->R; ++q) b.recv_off[q] = D->recv_off[q];
+  std::memcpy(blob, &b, sizeof(b));
+  return PJDS_OK;
+}
+
+int pjds_dist_p2p_connect(pjds_dist_t D, const void* blobs, int64_t blob_bytes) {
+  if (!D || !blobs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_connect: NULL argument");
+  if (D->transport != PJDS_TRANSPORT_P2P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_connect: not a P2P handle");
+  if (blob_bytes != (int64_t)sizeof(P2PBlob)) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_connect: blob size");
+  const P2PBlob* b = (const P2PBlob*)blobs;
+  for (int q = 0; q < D->R; ++q)
+    if (b[q].R != D->R || b[q].rank != q) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_connect: blobs not rank-ordered");
+  auto open = [&](int q) -> int {
+    if (D->peer_regions[q]) return PJDS_OK;
+    if (q == D->rank) {
+      D->peer_regions[q] = nullptr;
+      return PJDS_OK;
+    }
+    void* p = nullptr;
+    PJDS_CUDA_TRY(cudaIpcOpenMemHandle(&p, b[q].handle, cudaIpcMemLazyEnablePeerAccess));
+    D->peer_regions[q] = p;
+    return PJDS_OK;
+  };
+  const size_t vs = vsz(D);
+  std::vector<void*> dst0, dst1;
+  std::vector<uint64_t*> ready_t, done_t;
+  for (int q : D->send_peers) {  // my data goes to q's halo at q's offset for owner = me
+    PJDS_TRY(open(q));
+    char* base = (char*)D->peer_regions[q];
+    const size_t off = (size_t)b[q].recv_off[D->rank] * vs;
+    dst0.push_back(base + off);
+    dst1.push_back(base + b[q].halo_bytes + off);
+    ready_t.push_back((uint64_t*)(base + 2 * b[q].halo_bytes) + D->rank);
+  }
+  for (int p : D->recv_peers) {  // tell p when I am done reading its data
+    PJDS_TRY(open(p));
+    char* base = (char*)D->peer_regions[p];
+    done_t.push_back((uint64_t*)(base + 2 * b[p].halo_bytes) + D->R + D->rank);
+  }
+  if (!dst0.empty()) {
+    PJDS_CUDA_TRY(cudaMemcpy(D->d_dst[0], dst0.data(), dst0.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    PJDS_CUDA_TRY(cudaMemcpy(D->d_dst[1], dst1.data(), dst1.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    PJDS_CUDA_TRY(cudaMemcpy(D->d_ready_targets, ready_t.data(), ready_t.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  }
+  if (!done_t.empty())
+    PJDS_CUDA_TRY(cudaMemcpy(D->d_done_targets, done_t.data(), done_t.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  D->p2p_connected = true;
+  return PJDS_OK;
+}
+
+int pjds_dist_p2p_check(pjds_dist_t D, int32_t* timed_out) {
+  if (!D || !timed_out) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_check: NULL argument");
+  if (D->transport != PJDS_TRANSPORT_P2P) {
+    *timed_out = 0;
+    return PJDS_OK;
+  }
+  unsigned e = 0;
+  PJDS_CUDA_TRY(cudaMemcpy(&e, D->err_flag(), sizeof(e), cudaMemcpyDeviceToHost));
+  *timed_out = (int32_t)e;
   return PJDS_OK;
 }
 
@@ -476,7 +621,7 @@ int pjds_dist_parts(pjds_dist_t D, pjds_t* a, pjds_t* b) {
 int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t flags) {
   if (!D || (D->n_loc > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: NULL argument");
   if (y == x && D->n_loc > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: y aliases x");
-  if (D->transport != PJDS_TRANSPORT_NCCL) return set_error(PJDS_ERR_INVALID_ARG, "use pjds_dist_group_spmv for LOCAL transport");
+  if (D->transport == PJDS_TRANSPORT_LOCAL) return set_error(PJDS_ERR_INVALID_ARG, "use pjds_dist_group_spmv for LOCAL transport");
   cudaStream_t s = (cudaStream_t)stream;
   const bool comm_needed = D->R > 1 && (!D->sends.empty() || !D->recvs.empty());
   const bool tr = flags & PJDS_TRACE;
@@ -490,6 +635,40 @@ int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t
     for (int i = 0; i < 4; ++i) PJDS_TRY(mark(i, s));
     PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
     for (int i = 4; i < 7; ++i) PJDS_TRY(mark(i, s));
+    D->traced = D->traced || tr;
+    return PJDS_OK;
+  }
+  if (D->transport == PJDS_TRANSPORT_P2P) {
+    // fused local gather + put into the receivers' halo buffers, flag signalling (p2p.cu)
+    if (!D->p2p_connected) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: call pjds_dist_p2p_connect first");
+    const uint64_t sq = ++D->seq;
+    const int b = (int)(sq & 1);
+    const bool vec = flags & PJDS_NO_OVERLAP;
+    cudaStream_t cs = vec ? s : D->comm;
+    const int ns = (int)D->send_peers.size(), nr = (int)D->recv_peers.size();
+    PJDS_TRY(mark(0, s));
+    if (!vec) {
+      PJDS_CUDA_TRY(cudaEventRecord(D->ev_ready, s));
+      PJDS_CUDA_TRY(cudaStreamWaitEvent(cs, D->ev_ready, 0));
+    }
+    PJDS_TRY(mark(1, cs));
+    if (sq >= 3) PJDS_TRY(p2p_launch_wait(D->done_flags(), D->d_send_peers, ns, sq - 2, D->err_flag(), cs));
+    PJDS_TRY(p2p_launch_pack_put(x, D->d_p2p_idx, D->d_p2p_seg, D->d_dst[b], ns, D->p2p_max_count, D->dtype, cs));
+    PJDS_TRY(mark(2, cs));
+    PJDS_TRY(p2p_launch_signal(D->d_ready_targets, ns, sq, cs));
+    if (vec) PJDS_TRY(p2p_launch_wait(D->ready_flags(), D->d_recv_peers, nr, sq, D->err_flag(), s));
+    PJDS_TRY(mark(3, cs));
+    if (!vec) PJDS_CUDA_TRY(cudaEventRecord(D->ev_comm, cs));
+    PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));
+    PJDS_TRY(mark(4, s));
+    if (!vec) {
+      PJDS_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_comm, 0));  // own gather done: x may be reused
+      PJDS_TRY(p2p_launch_wait(D->ready_flags(), D->d_recv_peers, nr, sq, D->err_flag(), s));
+    }
+    PJDS_TRY(mark(5, s));
+    if (D->A_nl) PJDS_TRY(launch_pjds_spmv(D->A_nl, y, D->p2p_region + b * D->p2p_halo_bytes, s, true));
+    PJDS_TRY(p2p_launch_signal(D->d_done_targets, nr, sq, s));
+    PJDS_TRY(mark(6, s));
     D->traced = D->traced || tr;
     return PJDS_OK;
   }

@@ -93,6 +93,11 @@ int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, 
 // y = A x (permuted basis) plus per-CTA partials of y.x into part[0 .. *nparts); part must hold
 // n_pad / 256 + 1 doubles (the largest grid of any variant)
 int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t s, double* part, int64_t* nparts);
+// P2P transport kernels (p2p.cu)
+int p2p_launch_wait(const uint64_t* flags, const int* peers, int np, uint64_t target, unsigned* err, cudaStream_t s);
+int p2p_launch_signal(uint64_t* const* targets, int nt, uint64_t value, cudaStream_t s);
+int p2p_launch_pack_put(const void* x, const int* idx, const int64_t* seg, void* const* dst, int npeers,
+                        int64_t max_count, int dtype, cudaStream_t s);
 int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s);
 int launch_permute(const int32_t* perm, int64_t n, const void* src, void* dst, int dtype, int back, cudaStream_t s);
 int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int dtype, cudaStream_t s);

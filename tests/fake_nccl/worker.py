@@ -10,6 +10,8 @@ rank = int(os.environ["RANK"]); R = int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(0)
 dist.init_process_group("gloo")
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
+transport = sys.argv[2] if len(sys.argv) > 2 else "nccl"
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 if name == "rand":
     n, rp, col, val = inputs.small("random", 3000, seed=3, max=60)
 else:
@@ -22,7 +24,8 @@ x = inputs.vector(n)
 out = {}
 for permuted in (False, True):
     try:
-        D = pj.DistPjds.create(n, offs, rp[lo:hi + 1] - rp[lo], col[rp[lo]:rp[hi]], val[rp[lo]:rp[hi]], permuted=permuted)
+        D = pj.DistPjds.create(n, offs, rp[lo:hi + 1] - rp[lo], col[rp[lo]:rp[hi]], val[rp[lo]:rp[hi]],
+                               permuted=permuted, transport=transport)
     except Exception as e:
         print(json.dumps({"rank": rank, "create_error": str(e)[:300]})); sys.exit(0)
     xt = torch.from_numpy(x[lo:hi].copy()).cuda()
@@ -30,7 +33,8 @@ for permuted in (False, True):
         xt = D.to_permuted(torch.empty_like(xt), xt)
     for no in (False, True):
         y = torch.full_like(xt, float("nan"))
-        D.spmv(y, xt, no_overlap=no, trace=True)
+        for _ in range(reps):  # several calls: exercises the double-buffered halo / flag sequence
+            D.spmv(y, xt, no_overlap=no, trace=True)
         if permuted:
             y = D.from_permuted(torch.empty_like(y), y)
         torch.cuda.synchronize()
@@ -41,7 +45,8 @@ for permuted in (False, True):
         yl, b = oracle.spmv_ld(n, rp, col, val, x)
         ok = bool(oracle.acceptance(yall, yl, b, np.diff(rp), np.float64).all())
         out[f"perm{int(permuted)}_noov{int(no)}"] = {"o2": ok, "bitwise_vs_split_oracle": bool(np.array_equal(yall, ref)) if ref is not None else None,
-                                                     "trace": D.trace(), "halo": D.info["halo"], "messages": D.info["send_messages"]}
+                                                     "trace": D.trace(), "halo": D.info["halo"], "messages": D.info["send_messages"],
+                                                     "timed_out": D.p2p_timed_out()}
     D.close()
 print(json.dumps({"rank": rank, **out}))
 dist.destroy_process_group()

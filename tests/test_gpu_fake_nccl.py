@@ -25,6 +25,34 @@ def build_fake():
     return out
 
 
+def run_workers(case, R, transport, reps, port):
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    if transport == "nccl":
+        env["PJDS_NCCL_LIB"] = build_fake()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={R}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(HERE, "worker.py"), case, transport,
+           str(reps)]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and len(lines) == R, p.stdout[-2000:] + p.stderr[-3000:]
+    for rec in lines:
+        assert "create_error" not in rec, rec
+        for mode in ("perm0_noov0", "perm0_noov1", "perm1_noov0", "perm1_noov1"):
+            assert rec[mode]["o2"], (rec["rank"], mode)
+            assert rec[mode]["bitwise_vs_split_oracle"], (rec["rank"], mode)
+            assert not rec[mode]["timed_out"], (rec["rank"], mode)
+
+
+@pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4)])
+def test_p2p_transport_multiprocess_one_gpu(case, R):
+    """PJDS_TRANSPORT_P2P (fused gather+put into IPC-mapped peer halos, flag ordering), several calls
+    per mode so both halo buffers and the done/ready sequence are exercised."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    run_workers(case, R, "p2p", 5, 29740 + R + (10 if case == "rand" else 0))
+
+
 @pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4)])
 def test_nccl_transport_multiprocess_one_gpu(case, R):
     torch = pytest.importorskip("torch")
