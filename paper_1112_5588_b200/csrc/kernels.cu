@@ -133,9 +133,9 @@ template <> struct Vec<int, 4> {
 
 constexpr int kThreads = 256;
 constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
-#ifndef PJDS_MINB
-#define PJDS_MINB 1  // measured: capping registers for 6 CTAs/SM (<= 40 regs) is 3-15 % slower in DP
-#endif
+// Register budget: plain __launch_bounds__(256) (48 registers for the R=4 DP kernel).  Measured:
+// __launch_bounds__(256, 6) (<= 40 regs) is 3-15 % slower in DP, and __launch_bounds__(256, 1)
+// lets ptxas take 84 registers, halving occupancy (C2 DP 58 -> 147 us).
 
 // Store modes: y[perm[k]] = acc (row-only basis), y[k] = acc (permuted basis, PJDS_PERM_SYMMETRIC),
 // y[perm[k]] += acc (dist nonlocal part: the result is written twice).
@@ -152,7 +152,7 @@ enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 
 // chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
 template <typename T, typename Off, int R, int U, int MODE, bool PIPE>
-__global__ void __launch_bounds__(kThreads, PJDS_MINB)
+__global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
@@ -328,7 +328,8 @@ int set_tile_order_impl(int mode) {
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
 
 template <typename T, typename Off, int R, int U>
-int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part, int64_t* nparts) {
+int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part, int64_t* nparts,
+                  bool pipe) {
   const auto& h = A->h;
   const int64_t threads = h.n_pad / R;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
@@ -345,7 +346,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part)
 #define PJDS_LAUNCH(M)             \
-  if (g_pipe) PJDS_LAUNCH_PF(M, true); \
+  if (pipe) PJDS_LAUNCH_PF(M, true); \
   else PJDS_LAUNCH_PF(M, false)
   if (mode == STORE_DIRECT) {
     PJDS_LAUNCH(STORE_DIRECT);
@@ -370,6 +371,7 @@ static bool g_force_off64 = false;  // test hook: exercise the 64-bit offset ker
 template <typename T, typename Off>
 int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode, double* dp, int64_t* np) {
   int R = g_var_r, U = g_var_u;
+  bool pipe = g_pipe;
   if (R == 0) {
     // enough warps to cover the SMs several times: R = 4 (256-bit DP loads) for large matrices,
     // R = 2 / 1 when n_pad / R would leave the GPU short of warps (long-row matrices like DLR1)
@@ -377,17 +379,20 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
     if (np / 4 >= (int64_t(1) << 19)) { R = 4; U = 2; }
     else if (np / 2 >= (int64_t(1) << 17)) { R = 2; U = 4; }
     else { R = 1; U = 8; }
+    // long rows in SP (half the bytes per load): overlapping the next chunk's stream with the
+    // current gathers pays (measured C4 SP +5 %, W4 SP +10 %; DP on C4 loses, so DP stays plain)
+    pipe = sizeof(T) == 4 && R == 2;
   }
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;
   const T* xx = (const T*)x;
   if (R == 4)
-    return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np)
-                  : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode, dp, np);
+    return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np, pipe)
+                  : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode, dp, np, pipe);
   if (R == 2)
-    return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np)
-                  : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode, dp, np);
-  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode, dp, np);
+    return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np, pipe)
+                  : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode, dp, np, pipe);
+  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode, dp, np, pipe);
 }
 
 template <typename T>

@@ -6,6 +6,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 import inputs
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _nvh = pynvml.nvmlDeviceGetHandleByIndex(0)
+except Exception:
+    _nvh = None
+
+
+def clocks():
+    if _nvh is None:
+        return None
+    return (pynvml.nvmlDeviceGetClockInfo(_nvh, pynvml.NVML_CLOCK_SM), pynvml.nvmlDeviceGetClockInfo(_nvh, pynvml.NVML_CLOCK_MEM),
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(_nvh), pynvml.nvmlDeviceGetTemperature(_nvh, 0))
 import paper_1112_5588_b200 as pj
 
 p = argparse.ArgumentParser()
@@ -48,10 +61,11 @@ for cfg in a.configs.split(","):
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(a.reps): A.spmv(y, x)
+            ck = clocks()
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
             print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
-                              "stored_bytes": A.info.get("bytes_total")}), flush=True)
+                              "stored_bytes": A.info.get("bytes_total"), "clk": ck}), flush=True)
           del A
         del rp, col, val
