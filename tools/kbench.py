@@ -32,6 +32,7 @@ p.add_argument("--orders", default="2")
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
+pj.bw_probe(1 << 30, 20)  # bring the GPU out of its idle clocks before the first measurement
 for cfg in a.configs.split(","):
     for dts in a.dtypes.split(","):
         npdt = np.float64 if dts == "f64" else np.float32
