@@ -75,6 +75,17 @@ enum {
  */
 int pjds_create_from_crs(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col,
                          const void* val, int dtype, int32_t block_rows, uint32_t flags);
+/*
+ * pjds_create_from_crs_ex — as pjds_create_from_crs with a sort scope `sigma` (SURVEY §8(f)
+ * NEXT-2, the sliced-ELLPACK / SELL-C-sigma idea the paper names as future comparison, PAPER.md
+ * L527-531): rows are sorted by descending length only within consecutive windows of sigma rows,
+ * each window is padded and stored jagged column-major on its own (per-window col_start), so the
+ * permutation never moves a row out of its window (RHS locality).
+ * sigma = 0: one global window (the paper's pJDS).  Otherwise a multiple of 1024 and of block_rows.
+ */
+int pjds_create_from_crs_ex(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col,
+                            const void* val, int dtype, int32_t block_rows, int64_t sigma,
+                            uint32_t flags);
 int pjds_destroy(pjds_t A);
 
 /*
@@ -117,16 +128,24 @@ typedef struct {
   double data_reduction_vs_ellpack; /* 1 - stored / (ceil(n/32)*32 * width), entries basis */
   int32_t on_device;
   int32_t device;
+  int64_t sigma;          /* sort scope in rows (n_pad for the paper's global sort) */
+  int64_t n_windows;      /* number of sort windows (1 for the global sort) */
+  int64_t col_start_len;  /* entries of the concatenated per-window col_start (width+1 if global) */
 } pjds_info_t;
 
 int pjds_info(pjds_t A, pjds_info_t* out);
+
+/* Window layout (host buffers of n_windows+1 entries): wstart[w] = first stored slot of window w
+   (wstart[n_windows] = stored); wcs_off[w] = start of window w's col_start in the export array. */
+int pjds_export_windows(pjds_t A, int64_t* wstart, int64_t* wcs_off);
 
 /* Row-length histogram (Fig. 3, bin size 1): counts[L] = #rows of length L
    for L < nbins (rows longer than nbins-1 are not counted). */
 int pjds_histogram(pjds_t A, int64_t* counts, int32_t nbins);
 
 /* Copy the format arrays into caller HOST buffers sized from pjds_info: perm[n],
-   block_len[n_blocks], col_start[width+1], col[stored], val[stored] (any may be NULL). */
+   block_len[n_blocks], col_start[col_start_len] (per window, relative to the window's first
+   stored slot, concatenated), col[stored], val[stored] (any may be NULL). */
 int pjds_export(pjds_t A, int32_t* perm, int32_t* block_len, int64_t* col_start, int32_t* col,
                 void* val);
 

@@ -66,6 +66,63 @@ def pjds_reference(n, rowptr, col, val, b_r: int = 32, symmetric: bool = False):
                 b_r=b_r, row_len_sorted=sorted_len)
 
 
+def pjds_windows_reference(n, rowptr, col, val, b_r: int = 32, sigma: int = 1024, symmetric: bool = False):
+    """Sort scope sigma (the sliced-ELLPACK idea of PAPER.md L527-531): every
+    window of sigma consecutive rows is an independent pJDS matrix (pjds_reference on its rows),
+    stored one after the other.  Returns the concatenation plus wstart (first stored slot of each
+    window) and wcs_off (start of each window's col_start in the concatenated col_start)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    col = np.asarray(col)
+    val = np.asarray(val)
+    n_blocks = -(-n // b_r)
+    n_pad = n_blocks * b_r
+    if sigma <= 0 or sigma >= n_pad:
+        P = pjds_reference(n, rowptr, col, val, b_r=b_r, symmetric=symmetric)
+        P.update(wstart=np.array([0, P["stored"]], np.int64), wcs_off=np.array([0, P["width"] + 1], np.int64))
+        return P
+    parts = []
+    for r0 in range(0, n_pad, sigma):
+        r1 = min(n, r0 + sigma)
+        m = max(r1 - r0, 0)
+        sub_rp = rowptr[r0:r0 + m + 1] - rowptr[r0]
+        W = pjds_reference(m, sub_rp, col[rowptr[r0]:rowptr[r0 + m]], val[rowptr[r0]:rowptr[r0 + m]], b_r=b_r)
+        # the window's own padded row count (the last window may hold fewer blocks)
+        nb_w = (min(n_pad, r0 + sigma) - r0) // b_r
+        bl = np.zeros(nb_w, np.int32)
+        bl[:W["n_blocks"]] = W["block_len"]
+        W["block_len"] = bl
+        W["perm"] = W["perm"] + r0
+        parts.append(W)
+    perm = np.concatenate([W["perm"] for W in parts]).astype(np.int32)
+    invperm = np.empty(n, np.int32)
+    invperm[perm] = np.arange(n, dtype=np.int32)
+    out_col = np.concatenate([W["col"] for W in parts]).astype(np.int32)
+    if symmetric and len(out_col):
+        # padded slots keep column 0; real slots map through the global inverse permutation
+        is_real = np.concatenate([_real_slots(W) for W in parts])
+        out_col[is_real] = invperm[out_col[is_real]]
+    stored = [W["stored"] for W in parts]
+    wstart = np.zeros(len(parts) + 1, np.int64)
+    np.cumsum(stored, out=wstart[1:])
+    wcs_off = np.zeros(len(parts) + 1, np.int64)
+    np.cumsum([W["width"] + 1 for W in parts], out=wcs_off[1:])
+    return dict(perm=perm, invperm=invperm, block_len=np.concatenate([W["block_len"] for W in parts]),
+                col_start=np.concatenate([W["col_start"] for W in parts]), val=np.concatenate([W["val"] for W in parts]),
+                col=out_col, n=n, n_pad=n_pad, n_blocks=n_blocks, width=max(W["width"] for W in parts),
+                stored=int(wstart[-1]), b_r=b_r, wstart=wstart, wcs_off=wcs_off, sigma=sigma)
+
+
+def _real_slots(W):
+    """Boolean mask over a pJDS matrix's slots: True where the slot holds a stored CRS entry."""
+    mask = np.zeros(W["stored"], bool)
+    lens = W["row_len_sorted"]
+    for j in range(W["width"]):
+        m = int(W["col_start"][j + 1] - W["col_start"][j])
+        k = np.arange(m)
+        mask[W["col_start"][j] + k] = lens[k] > j
+    return mask
+
+
 def ellr_reference(n, rowptr, col, val, warp: int = 32):
     """CRS -> ELLPACK-R, PAPER.md L146-159 (shift left, N x N^max rectangle, column-major,
     N padded to a multiple of the warp size, footnote L153-155) and L187-191 (rowmax[]).

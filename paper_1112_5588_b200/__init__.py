@@ -75,12 +75,14 @@ class PjdsMatrix:
         self.dtype = self.info["dtype"]
 
     @classmethod
-    def from_crs(cls, n, rowptr, col, val, block_rows: int = 32, symmetric: bool = False, host_only: bool = False):
+    def from_crs(cls, n, rowptr, col, val, block_rows: int = 32, symmetric: bool = False, host_only: bool = False,
+                 sigma: int = 0):
+        """sigma: sort scope in rows (0 = the paper's global sort; else a multiple of 1024)."""
         rowptr, col, val = _crs(rowptr, col, val)
         flags = (PJDS_PERM_SYMMETRIC if symmetric else 0) | (PJDS_HOST_ONLY if host_only else 0)
         h = ctypes.c_void_p()
-        call("pjds_create_from_crs", ctypes.byref(h), int(n), rowptr.ctypes.data, col.ctypes.data, val.ctypes.data,
-             _dt(val), int(block_rows), flags)
+        call("pjds_create_from_crs_ex", ctypes.byref(h), int(n), rowptr.ctypes.data, col.ctypes.data,
+             val.ctypes.data, _dt(val), int(block_rows), int(sigma), flags)
         return cls(h)
 
     def close(self):
@@ -139,10 +141,12 @@ class PjdsMatrix:
     def export(self):
         i = self.info
         out = dict(perm=np.empty(i["n"], np.int32), block_len=np.empty(i["n_blocks"], np.int32),
-                   col_start=np.empty(i["width"] + 1, np.int64), col=np.empty(i["stored"], np.int32),
-                   val=np.empty(i["stored"], _np_dtype(i["dtype"])))
+                   col_start=np.empty(i["col_start_len"], np.int64), col=np.empty(i["stored"], np.int32),
+                   val=np.empty(i["stored"], _np_dtype(i["dtype"])),
+                   wstart=np.empty(i["n_windows"] + 1, np.int64), wcs_off=np.empty(i["n_windows"] + 1, np.int64))
         call("pjds_export", self._h, out["perm"].ctypes.data, out["block_len"].ctypes.data,
              out["col_start"].ctypes.data, out["col"].ctypes.data, out["val"].ctypes.data)
+        call("pjds_export_windows", self._h, out["wstart"].ctypes.data, out["wcs_off"].ctypes.data)
         return out
 
 

@@ -24,7 +24,8 @@ class PjdsInfo(ctypes.Structure):
                 ("len_min", c_i32), ("len_max", c_i32), ("len_mean", c_dbl),
                 ("useful_fma", c_i64), ("padded_fma", c_i64), ("idle_lane_slots", c_i64),
                 ("bytes_values", c_i64), ("bytes_indices", c_i64), ("bytes_aux", c_i64), ("bytes_total", c_i64),
-                ("data_reduction_vs_ellpack", c_dbl), ("on_device", c_i32), ("device", c_i32)]
+                ("data_reduction_vs_ellpack", c_dbl), ("on_device", c_i32), ("device", c_i32),
+                ("sigma", c_i64), ("n_windows", c_i64), ("col_start_len", c_i64)]
 
 
 class EllrInfo(ctypes.Structure):
@@ -52,6 +53,8 @@ def struct_dict(s) -> dict:
 
 _SIGS = {
     "pjds_create_from_crs": [c_p, c_i64, c_p, c_p, c_p, ctypes.c_int, c_i32, c_u32],
+    "pjds_create_from_crs_ex": [c_p, c_i64, c_p, c_p, c_p, ctypes.c_int, c_i32, c_i64, c_u32],
+    "pjds_export_windows": [c_p, c_p, c_p],
     "pjds_destroy": [c_p],
     "pjds_spmv": [c_p, c_p, c_p, c_p],
     "pjds_spmv_host": [c_p, c_p, c_p, c_p],

@@ -1,4 +1,5 @@
 // C ABI of libpjds (include/pjds.h): single-GPU pJDS / ELLPACK-R handles.
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include "internal.h"
@@ -22,7 +23,8 @@ static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
 
 int free_pjds_device(pjds_mat* A) {
   cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
-  cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys);
+  cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off);
+  A->d_wcs_off = nullptr;
   for (auto& o : A->d_order) {
     cudaFree(o);
     o = nullptr;
@@ -46,10 +48,21 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
     for (int64_t k = 0; k < h.n; ++k) target[k] = store_map[h.perm[k]];
     tp = target.data();
   }
+  // kernel view of col_start: per window w, wstart[w] + col_start_w[j] - w * sigma, so that the
+  // slot of sorted row k in column j is cs[j] + k for every window
+  std::vector<int64_t> cs_abs(h.col_start.size());
+  for (int64_t w = 0; w < std::max<int64_t>(h.n_windows, 1); ++w) {
+    const int64_t a0 = h.wcs_off.empty() ? 0 : h.wcs_off[w];
+    const int64_t a1 = h.wcs_off.empty() ? (int64_t)cs_abs.size() : h.wcs_off[w + 1];
+    const int64_t add = (h.wstart.empty() ? 0 : h.wstart[w]) - w * h.sigma;
+    for (int64_t i = a0; i < a1; ++i) cs_abs[i] = h.col_start[i] + add;
+  }
+  std::vector<int64_t> woff = h.wcs_off.empty() ? std::vector<int64_t>{0, (int64_t)cs_abs.size()} : h.wcs_off;
   int s = PJDS_OK;
   if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
       (s = dmalloc_copy(&A->d_col, h.col.data(), h.col.size() * 4)) ||
-      (s = dmalloc_copy(&A->d_col_start, h.col_start.data(), h.col_start.size() * 8)) ||
+      (s = dmalloc_copy(&A->d_col_start, cs_abs.data(), cs_abs.size() * 8)) ||
+      (s = dmalloc_copy(&A->d_wcs_off, woff.data(), woff.size() * 8)) ||
       (s = dmalloc_copy(&A->d_block_len, h.block_len.data(), h.block_len.size() * 4)) ||
       (s = dmalloc_copy(&A->d_perm, tp, (size_t)h.n * 4))) {
     free_pjds_device(A);
@@ -70,8 +83,16 @@ extern "C" {
 const char* pjds_last_error(void) { return g_err.c_str(); }
 const char* pjds_version(void) { return "libpjds 0.1 (sm_100a)"; }
 
+int pjds_create_from_crs_ex(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                            int dtype, int32_t block_rows, int64_t sigma, uint32_t flags);
+
 int pjds_create_from_crs(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
                          int dtype, int32_t block_rows, uint32_t flags) {
+  return pjds_create_from_crs_ex(out, n, rowptr, col, val, dtype, block_rows, 0, flags);
+}
+
+int pjds_create_from_crs_ex(pjds_t* out, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                            int dtype, int32_t block_rows, int64_t sigma, uint32_t flags) {
   if (!out) return set_error(PJDS_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (flags & ~(uint32_t)(PJDS_PERM_SYMMETRIC | PJDS_HOST_ONLY)) return set_error(PJDS_ERR_INVALID_ARG, "unknown flags");
@@ -79,7 +100,7 @@ int pjds_create_from_crs(pjds_t* out, int64_t n, const int64_t* rowptr, const in
   pjds_mat* A = new (std::nothrow) pjds_mat();
   if (!A) return set_error(PJDS_ERR_OOM, "handle allocation failed");
   A->flags = flags;
-  int s = convert_pjds(A->h, n, n, rowptr, col, val, dtype, block_rows, flags & PJDS_PERM_SYMMETRIC);
+  int s = convert_pjds(A->h, n, n, rowptr, col, val, dtype, block_rows, flags & PJDS_PERM_SYMMETRIC, sigma);
   if (s == PJDS_OK && !(flags & PJDS_HOST_ONLY)) {
     if (flags & PJDS_PERM_SYMMETRIC) {
       // permuted basis: y_perm[k] is stored at k; the kernel does not read perm at all
@@ -165,12 +186,24 @@ int pjds_info(pjds_t A, pjds_info_t* o) {
   o->idle_lane_slots = 0;
   o->bytes_values = h.stored * (int64_t)dtype_size(h.dtype);
   o->bytes_indices = h.stored * 4;
-  o->bytes_aux = (int64_t)(h.width + 1) * 8 + h.n_blocks * 4 + h.n * 4;
+  o->bytes_aux = (int64_t)h.col_start.size() * 8 + h.n_blocks * 4 + h.n * 4 +
+                 (h.n_windows > 1 ? (h.n_windows + 1) * 16 : 0);
   o->bytes_total = o->bytes_values + o->bytes_indices + o->bytes_aux;
   const int64_t ell = (h.n + 31) / 32 * 32 * (int64_t)h.width;
   o->data_reduction_vs_ellpack = ell ? 1.0 - (double)h.stored / (double)ell : 0.0;
   o->on_device = A->on_device;
   o->device = A->device;
+  o->sigma = h.sigma;
+  o->n_windows = h.n_windows;
+  o->col_start_len = (int64_t)h.col_start.size();
+  return PJDS_OK;
+}
+
+int pjds_export_windows(pjds_t A, int64_t* wstart, int64_t* wcs_off) {
+  if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_export_windows: NULL handle");
+  const auto& h = A->h;
+  if (wstart) std::memcpy(wstart, h.wstart.data(), h.wstart.size() * 8);
+  if (wcs_off) std::memcpy(wcs_off, h.wcs_off.data(), h.wcs_off.size() * 8);
   return PJDS_OK;
 }
 
@@ -185,7 +218,7 @@ int pjds_export(pjds_t A, int32_t* perm, int32_t* block_len, int64_t* col_start,
   const auto& h = A->h;
   if (perm) std::memcpy(perm, h.perm.data(), (size_t)h.n * 4);
   if (block_len) std::memcpy(block_len, h.block_len.data(), (size_t)h.n_blocks * 4);
-  if (col_start) std::memcpy(col_start, h.col_start.data(), (size_t)(h.width + 1) * 8);
+  if (col_start) std::memcpy(col_start, h.col_start.data(), h.col_start.size() * 8);
   const size_t vb = (size_t)h.stored * dtype_size(h.dtype);
   if (A->on_device) {
     if (col) PJDS_CUDA_TRY(cudaMemcpy(col, A->d_col, (size_t)h.stored * 4, cudaMemcpyDeviceToHost));

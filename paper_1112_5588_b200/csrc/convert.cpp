@@ -73,9 +73,11 @@ void sort_rows(int64_t n, const int32_t* len, int32_t maxlen, int32_t* perm) {
 }  // namespace
 
 int convert_pjds(PjdsHost& o, int64_t n, int64_t ncols, const int64_t* rowptr, const int32_t* col,
-                 const void* val, int dtype, int32_t br, bool symmetric) {
+                 const void* val, int dtype, int32_t br, bool symmetric, int64_t sigma) {
   if (dtype != PJDS_F32 && dtype != PJDS_F64) return set_error(PJDS_ERR_INVALID_ARG, "dtype must be PJDS_F32 or PJDS_F64");
   if (br <= 0 || br % 32 != 0) return set_error(PJDS_ERR_INVALID_ARG, "block_rows must be a positive multiple of 32");
+  if (sigma < 0 || (sigma > 0 && (sigma % 1024 != 0 || sigma % br != 0)))
+    return set_error(PJDS_ERR_INVALID_ARG, "sigma must be 0 (global sort) or a multiple of 1024 and of block_rows");
   if (symmetric && ncols != n) return set_error(PJDS_ERR_INVALID_ARG, "symmetric permutation needs a square matrix");
   PJDS_TRY(validate_crs(n, ncols, rowptr, col));
   const int64_t nnz = rowptr[n];
@@ -96,25 +98,46 @@ int convert_pjds(PjdsHost& o, int64_t n, int64_t ncols, const int64_t* rowptr, c
     o.len_max = mx; o.len_min = mn;
     o.hist.assign((size_t)mx + 1, 0);
     for (int64_t i = 0; i < n; ++i) o.hist[len[i]]++;
-    // a2 sort
-    o.perm.resize(n);
-    if (n) sort_rows(n, len.data(), mx, o.perm.data());
-    // a3 pad
+    // a2 sort (within windows of sigma rows; one window = the paper's global sort)
     o.n_blocks = (n + br - 1) / br;
     o.n_pad = o.n_blocks * br;
-    o.block_len.resize(o.n_blocks);
-    for (int64_t b = 0; b < o.n_blocks; ++b) o.block_len[b] = len[o.perm[b * br]];  // first row is longest
-    o.width = o.n_blocks ? o.block_len[0] : 0;
-    // a4 col_start: nb_gt[j] = #blocks with block_len > j (block_len is non-increasing)
-    std::vector<int64_t> nb_at((size_t)o.width + 2, 0);
-    for (int64_t b = 0; b < o.n_blocks; ++b) nb_at[o.block_len[b]]++;
-    o.col_start.assign((size_t)o.width + 1, 0);
-    int64_t gt = o.n_blocks - nb_at[0];  // blocks with len > 0
-    for (int32_t j = 0; j < o.width; ++j) {
-      o.col_start[j + 1] = o.col_start[j] + (int64_t)br * gt;
-      gt -= nb_at[j + 1];
+    o.sigma = (sigma <= 0 || sigma >= o.n_pad) ? std::max<int64_t>(o.n_pad, br) : sigma;
+    o.n_windows = o.n_pad ? (o.n_pad + o.sigma - 1) / o.sigma : 0;
+    o.perm.resize(n);
+    for (int64_t w = 0; w < o.n_windows; ++w) {
+      const int64_t r0 = w * o.sigma, r1 = std::min(n, r0 + o.sigma);
+      if (r1 <= r0) continue;
+      sort_rows(r1 - r0, len.data() + r0, mx, o.perm.data() + r0);
+      if (r0)
+        for (int64_t k = r0; k < r1; ++k) o.perm[k] += (int32_t)r0;
     }
-    o.stored = o.col_start[o.width];
+    // a3 pad: block_len[b] = length of the first (longest) row of block b in its window
+    o.block_len.resize(o.n_blocks);
+    for (int64_t b = 0; b < o.n_blocks; ++b) o.block_len[b] = b * br < n ? len[o.perm[b * br]] : 0;
+    // a4 col_start per window: nb_gt[j] = #blocks of the window with block_len > j (non-increasing)
+    o.wstart.assign(o.n_windows + 1, 0);
+    o.wcs_off.assign(o.n_windows + 1, 0);
+    o.col_start.clear();
+    o.width = 0;
+    const int64_t bpw = o.sigma / br;  // blocks per window
+    for (int64_t w = 0; w < o.n_windows; ++w) {
+      const int64_t b0 = w * bpw, b1 = std::min(o.n_blocks, b0 + bpw);
+      const int32_t ww = b1 > b0 ? o.block_len[b0] : 0;
+      o.width = std::max(o.width, ww);
+      std::vector<int64_t> nb_at((size_t)ww + 2, 0);
+      for (int64_t b = b0; b < b1; ++b) nb_at[o.block_len[b]]++;
+      const size_t base = o.col_start.size();
+      o.col_start.resize(base + ww + 1, 0);
+      int64_t gt = (b1 - b0) - nb_at[0];
+      for (int32_t j = 0; j < ww; ++j) {
+        o.col_start[base + j + 1] = o.col_start[base + j] + (int64_t)br * gt;
+        gt -= nb_at[j + 1];
+      }
+      o.wcs_off[w + 1] = (int64_t)o.col_start.size();
+      o.wstart[w + 1] = o.wstart[w] + o.col_start[base + ww];
+    }
+    if (o.n_windows == 0) o.col_start.assign(1, 0);
+    o.stored = o.wstart[o.n_windows];
     // a5 fill
     o.col.assign(o.stored, 0);
     o.val.assign((size_t)o.stored * vs, 0);  // +0.0 bit pattern for padding
@@ -124,17 +147,20 @@ int convert_pjds(PjdsHost& o, int64_t n, int64_t ncols, const int64_t* rowptr, c
 #pragma omp parallel for
       for (int64_t k = 0; k < n; ++k) inv[o.perm[k]] = (int32_t)k;
     }
-    const int64_t* cs = o.col_start.data();
     int32_t* oc = o.col.data();
     uint8_t* ov = o.val.data();
     const uint8_t* iv = (const uint8_t*)val;
+    const int64_t sg = o.sigma;
 #pragma omp parallel for schedule(static, 1024)
     for (int64_t k = 0; k < n; ++k) {
+      const int64_t w = k / sg;
+      const int64_t* cs = o.col_start.data() + o.wcs_off[w];
+      const int64_t kk = o.wstart[w] + (k - w * sg);  // slot of row k in jagged column 0 of its window
       const int64_t r = o.perm[k];
       const int64_t base = rowptr[r];
       const int32_t l = len[r];
       for (int32_t j = 0; j < l; ++j) {
-        const int64_t dst = cs[j] + k;
+        const int64_t dst = cs[j] + kk;
         const int32_t c = col[base + j];
         oc[dst] = symmetric ? inv[c] : c;
         std::memcpy(ov + dst * vs, iv + (base + j) * vs, vs);

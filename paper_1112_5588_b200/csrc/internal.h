@@ -32,7 +32,10 @@ struct PjdsHost {
   int32_t br = 32, width = 0, dtype = PJDS_F64, len_min = 0, len_max = 0;
   std::vector<int32_t> perm;       // [n]  perm[new] = old
   std::vector<int32_t> block_len;  // [n_blocks]
-  std::vector<int64_t> col_start;  // [width+1]
+  std::vector<int64_t> col_start;  // per window: [width_w+1] offsets relative to the window start
+  int64_t sigma = 0, n_windows = 0;  // sort scope (rows per window; n_pad = one global window)
+  std::vector<int64_t> wstart;     // [n_windows+1] first stored slot of each window
+  std::vector<int64_t> wcs_off;    // [n_windows+1] start of each window's col_start in col_start
   std::vector<int32_t> col;        // [stored]
   std::vector<uint8_t> val;        // [stored * dtype_size]
   std::vector<int64_t> hist;       // [len_max+1]
@@ -41,7 +44,7 @@ struct PjdsHost {
 // CRS (rows x ncols) -> pJDS host arrays.  `val_src` optional gather index (val[k] = val_in[src[k]]).
 // Validates CRS; cols must be < ncols.  symmetric: columns -> invperm[col] (requires ncols == n).
 int convert_pjds(PjdsHost& out, int64_t n, int64_t ncols, const int64_t* rowptr, const int32_t* col,
-                 const void* val, int dtype, int32_t br, bool symmetric);
+                 const void* val, int dtype, int32_t br, bool symmetric, int64_t sigma = 0);
 
 struct EllrHost {
   int64_t n = 0, nnz = 0, n_pad = 0, stored = 0, idle = 0;
@@ -64,7 +67,8 @@ struct pjds_mat {
   int device = -1;
   void* d_val = nullptr;
   int32_t* d_col = nullptr;
-  int64_t* d_col_start = nullptr;
+  int64_t* d_col_start = nullptr;  // per window: wstart[w] + col_start_w[j] - w*sigma (kernel view)
+  int64_t* d_wcs_off = nullptr;
   int32_t* d_block_len = nullptr;
   int32_t* d_perm = nullptr;  // store target per sorted row (orig row; or local row for A_nl)
   void* d_xs = nullptr;       // staging for pjds_spmv_host

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
-                 double* __restrict__ dot_part) {
+                 double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off) {
   __shared__ Off s_cs[kSmemCS];
   // execution order of the CTA tiles (storage order, or by original row; results are identical)
   const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
@@ -164,6 +164,9 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const int64_t k0 = t * R;
   const int64_t cta_k0 = tile * kThreads * R;
   const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
+  // sort window of this CTA (CTAs never straddle windows: sigma is a multiple of the tile size);
+  // its col_start table already includes the window's storage offset (kernel view)
+  col_start += wcs_off[cta_k0 / sigma];
   const int lim = min(cta_len + 1, kSmemCS);
   for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
   __syncthreads();
@@ -340,11 +343,13 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   // together) or when x does not fit comfortably in L2 (measured: C5 DP permuted +6 %, rows-only
   // +44 %; C2/C4, whose x fits L2, lose ~1 % with it, so they keep storage order)
   const bool by_row = g_tile_order == 1 ||
-                      (g_tile_order == 2 && (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
+                      (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
+                       (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(const_cast<pjds_mat*>(A), R, kThreads * R, grid, &order));
 #define PJDS_LAUNCH_PF(M, PF)                                                                            \
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
-      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part)
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part, h.sigma, \
+      A->d_wcs_off)
 #define PJDS_LAUNCH(M)             \
   if (pipe) PJDS_LAUNCH_PF(M, true); \
   else PJDS_LAUNCH_PF(M, false)

@@ -29,6 +29,7 @@ p.add_argument("--reps", type=int, default=30)
 p.add_argument("--variants", default="0x0")
 p.add_argument("--policies", default="1x2")
 p.add_argument("--orders", default="2")
+p.add_argument("--sigmas", default="0")
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
@@ -42,10 +43,11 @@ for cfg in a.configs.split(","):
         x = torch.from_numpy(inputs.vector(n, npdt)).cuda()
         y = torch.empty_like(x)
         bmin = nnz * (sv + 4) + 2 * n * sv
-        for fmt in a.fmts.split(","):
+        for fmt, sg in [(f, g) for f in a.fmts.split(",") for g in (a.sigmas.split(",") if f.startswith("pjds") else ["0"])]:
           if fmt.startswith("pjds"):
               sym = fmt.endswith("s")
-              A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=int(fmt[4:].rstrip("s")), symmetric=sym)
+              A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=int(fmt[4:].rstrip("s")), symmetric=sym,
+                                         sigma=int(sg))
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
           for var, polk, order in [(v, q, o) for v in a.variants.split(",") for q in a.policies.split(",") for o in a.orders.split(",")]:
@@ -65,7 +67,7 @@ for cfg in a.configs.split(","):
             ck = clocks()
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
-            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
                               "stored_bytes": A.info.get("bytes_total"), "clk": ck}), flush=True)
           del A
