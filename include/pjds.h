@@ -266,6 +266,9 @@ int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* out);
 int pjds_dist_trace(pjds_dist_t D, double* ms /* [6] */);
 /* The two pJDS parts (owned by D; do not destroy): A_loc, A_nl (A_nl may be NULL if empty). */
 int pjds_dist_parts(pjds_dist_t D, pjds_t* A_loc, pjds_t* A_nl);
+/* Frees the handle (and, for NCCL, the communicator; for P2P, the IPC mappings and the exported
+   region).  Collective in effect: synchronise all ranks' streams and barrier before destroying, so
+   no peer still writes into (P2P) or exchanges with (NCCL) this rank. */
 int pjds_dist_destroy(pjds_dist_t D);
 
 /* NCCL helpers (NCCL is dlopen-ed; `libpath` NULL tries "libnccl.so.2"). */

@@ -68,6 +68,10 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
     free_pjds_device(A);
     return s;
   }
+  if ((s = build_tile_orders(A)) != PJDS_OK) {
+    free_pjds_device(A);
+    return s;
+  }
   A->on_device = true;
   std::vector<int32_t>().swap(h.col);
   std::vector<uint8_t>().swap(h.val);

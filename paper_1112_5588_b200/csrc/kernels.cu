@@ -304,22 +304,9 @@ static int g_tile_order = 2;  // 0 storage order, 1 by first row's original inde
 // Tiles (CTAs of rows_per_tile consecutive sorted rows) ordered by the original index of their first
 // row: all length classes of one region of the original matrix run together, so the RHS entries
 // they share are reused from L2 (the sort destroys this locality).
-int tile_order_for(pjds_mat* A, int R, int64_t rows_per_tile, int64_t tiles, const int** out) {
-  int slot = R == 4 ? 2 : (R == 2 ? 1 : 0);
-  if (!A->d_order[slot]) {
-    const auto& h = A->h;
-    std::vector<int64_t> key(tiles);
-    for (int64_t t = 0; t < tiles; ++t) {
-      const int64_t k = t * rows_per_tile;
-      key[t] = k < h.n ? (int64_t)h.perm[k] : INT64_MAX;
-    }
-    std::vector<int32_t> ord(tiles);
-    for (int64_t t = 0; t < tiles; ++t) ord[t] = (int32_t)t;
-    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_order[slot], tiles * 4));
-    PJDS_CUDA_TRY(cudaMemcpy(A->d_order[slot], ord.data(), tiles * 4, cudaMemcpyHostToDevice));
-  }
-  *out = A->d_order[slot];
+int tile_order_for(const pjds_mat* A, int R, const int** out) {
+  *out = A->d_order[R == 4 ? 2 : (R == 2 ? 1 : 0)];
+  if (!*out) return set_error(PJDS_ERR_CUDA, "tile order table missing (handle not uploaded)");
   return PJDS_OK;
 }
 
@@ -345,7 +332,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   const bool by_row = g_tile_order == 1 ||
                       (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
                        (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
-  if (by_row) PJDS_TRY(tile_order_for(const_cast<pjds_mat*>(A), R, kThreads * R, grid, &order));
+  if (by_row) PJDS_TRY(tile_order_for(A, R, &order));
 #define PJDS_LAUNCH_PF(M, PF)                                                                            \
   pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part, h.sigma, \
@@ -490,6 +477,28 @@ __global__ void read_kernel(const int4* __restrict__ a, int64_t n, int* __restri
 }
 
 }  // namespace
+
+// Tiles (CTAs of 256 R consecutive sorted rows) ordered by the original index of their first row,
+// one table per rows-per-thread variant R in {1, 2, 4}; built once at upload.
+int build_tile_orders(pjds_mat* A) {
+  const auto& h = A->h;
+  const int Rs[3] = {1, 2, 4};
+  for (int slot = 0; slot < 3; ++slot) {
+    const int64_t rows = (int64_t)kThreads * Rs[slot];
+    const int64_t tiles = std::max<int64_t>((h.n_pad + rows - 1) / rows, 1);
+    std::vector<int64_t> key(tiles);
+    for (int64_t t = 0; t < tiles; ++t) {
+      const int64_t k = t * rows;
+      key[t] = k < h.n ? (int64_t)h.perm[k] : INT64_MAX;
+    }
+    std::vector<int32_t> ord(tiles);
+    for (int64_t t = 0; t < tiles; ++t) ord[t] = (int32_t)t;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_order[slot], tiles * 4));
+    PJDS_CUDA_TRY(cudaMemcpy(A->d_order[slot], ord.data(), tiles * 4, cudaMemcpyHostToDevice));
+  }
+  return PJDS_OK;
+}
 
 int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool accumulate) {
   const int mode = accumulate ? STORE_PERM_ACC : (A->direct_store ? STORE_DIRECT : STORE_PERM);

@@ -53,11 +53,10 @@ def test_no_spills_in_any_default_kernel(usage):
         assert local == 0, name
 
 
-def test_sass_has_256bit_evict_first_loads():
-    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                          "_ZN4pjds43_GLOBAL__N__89249713_10_kernels_cu_4292054216pjds_spmv_kernelIdiLi4ELi2ELi1ELb0EEEvPKT_PKiPKlS6_S6_S4_PS2_lliiS6_Pd",
-                          LIB], capture_output=True, text=True).stdout
-    if not out.strip():  # the mangled name embeds a per-build hash; fall back to a full dump
-        out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
-    assert re.search(r"LDG\.E(\.NA)?\.EFL2\.256", out), "no 256-bit evict-first LDG in the pJDS kernels"
+def test_sass_has_256bit_evict_first_loads(usage):
+    """The R=4 DP permuted-basis kernel streams val with 256-bit L1-no-allocate / L2-evict-first loads."""
+    name = next(k for k in usage if re.search(r"pjds_spmv_kernelIdiLi4ELi2ELi1ELb0E", k))
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun", name, LIB], capture_output=True,
+                         text=True).stdout
+    assert re.search(r"LDG\.E(\.NA)?\.EFL2\.256", out), "no 256-bit evict-first LDG in the pJDS kernel"
     assert re.search(r"LDG\.E\.NA\.", out), "no L1::no_allocate streaming loads"
