@@ -114,6 +114,16 @@ int pjds_permute(pjds_t A, void* dst, const void* src, int32_t direction, void* 
  */
 int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream);
 
+/*
+ * pjds_spmv_host_batch — `count` independent products y_host[i] = A x_host[i] with host vectors
+ * (original basis), pipelined: the host->device copy of x_{i+1} and the device->host copy of y_{i-1}
+ * run on two copy streams while product i runs on `stream` (double-buffered staging owned by the
+ * handle), so PCIe traffic in both directions overlaps the kernels.  Host vectors should be
+ * pinned for the copies to be asynchronous.  Synchronises `stream` before returning.
+ */
+int pjds_spmv_host_batch(pjds_t A, void* const* y_host, const void* const* x_host, int32_t count,
+                         void* stream);
+
 typedef struct {
   int64_t n, nnz, n_pad, n_blocks, stored;
   int32_t block_rows, width, dtype, flags;

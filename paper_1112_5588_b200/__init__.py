@@ -123,6 +123,18 @@ class PjdsMatrix:
         call("pjds_spmv_host", self._h, y.ctypes.data, x.ctypes.data, _stream_ptr(stream))
         return y
 
+    def spmv_host_batch(self, ys, xs, stream=None):
+        """Pipelined end-to-end products ys[i] = A xs[i] with (pinned) host numpy arrays in the original
+        basis: H2D of the next x and D2H of the previous y overlap the current product."""
+        nd = _np_dtype(self.dtype)
+        assert len(ys) == len(xs)
+        for v in list(xs) + list(ys):
+            assert v.dtype == nd and v.flags.c_contiguous and len(v) >= self.n
+        Y = (ctypes.c_void_p * len(ys))(*[v.ctypes.data for v in ys])
+        X = (ctypes.c_void_p * len(xs))(*[v.ctypes.data for v in xs])
+        call("pjds_spmv_host_batch", self._h, Y, X, len(xs), _stream_ptr(stream))
+        return ys
+
     def lanczos(self, v0, m: int, stream=None):
         """m Lanczos steps in the permuted basis (needs symmetric=True and a symmetric matrix).
         v0: CUDA tensor in the permuted basis.  Returns (alpha, beta, steps_done) as numpy."""

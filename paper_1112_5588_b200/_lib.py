@@ -58,6 +58,7 @@ _SIGS = {
     "pjds_destroy": [c_p],
     "pjds_spmv": [c_p, c_p, c_p, c_p],
     "pjds_spmv_host": [c_p, c_p, c_p, c_p],
+    "pjds_spmv_host_batch": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_permute": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_info": [c_p, c_p],
     "pjds_histogram": [c_p, c_p, c_i32],

@@ -25,6 +25,17 @@ int free_pjds_device(pjds_mat* A) {
   cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
   cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off);
   A->d_wcs_off = nullptr;
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(A->d_bx[b]); cudaFree(A->d_by[b]); cudaFree(A->d_bp[b]);
+    A->d_bx[b] = A->d_by[b] = A->d_bp[b] = nullptr;
+  }
+  if (A->s_h2d) cudaStreamDestroy(A->s_h2d);
+  if (A->s_d2h) cudaStreamDestroy(A->s_d2h);
+  A->s_h2d = A->s_d2h = nullptr;
+  for (auto& e : A->ev_b) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
   for (auto& o : A->d_order) {
     cudaFree(o);
     o = nullptr;
@@ -166,6 +177,56 @@ int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream) {
   }
   PJDS_CUDA_TRY(cudaMemcpyAsync(y_host, A->d_ys, bytes_y, cudaMemcpyDeviceToHost, s));
   PJDS_CUDA_TRY(cudaStreamSynchronize(s));
+  return PJDS_OK;
+}
+
+int pjds_spmv_host_batch(pjds_t A, void* const* y_host, const void* const* x_host, int32_t count, void* stream) {
+  if (!A || count < 0 || (count > 0 && (!y_host || !x_host)))
+    return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host_batch: bad argument");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host_batch: handle is host-only");
+  const size_t vs = dtype_size(A->h.dtype);
+  const size_t bx = std::max<size_t>((size_t)A->ncols * vs, 16), by = std::max<size_t>((size_t)A->h.n * vs, 16);
+  const bool sym = A->direct_store;
+  if (!A->d_bx[0]) {
+    for (int b = 0; b < 2; ++b) {
+      PJDS_CUDA_TRY(cudaMalloc(&A->d_bx[b], bx));
+      PJDS_CUDA_TRY(cudaMalloc(&A->d_by[b], by));
+      if (sym) PJDS_CUDA_TRY(cudaMalloc(&A->d_bp[b], std::max(bx, by)));
+    }
+    PJDS_CUDA_TRY(cudaStreamCreateWithFlags(&A->s_h2d, cudaStreamNonBlocking));
+    PJDS_CUDA_TRY(cudaStreamCreateWithFlags(&A->s_d2h, cudaStreamNonBlocking));
+    for (auto& e : A->ev_b) PJDS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaEvent_t *ev_x = A->ev_b, *ev_y = A->ev_b + 2, *ev_xf = A->ev_b + 4, *ev_yf = A->ev_b + 6, ev0 = A->ev_b[8];
+  // the copy streams start after everything already queued on the caller's stream
+  PJDS_CUDA_TRY(cudaEventRecord(ev0, cs));
+  PJDS_CUDA_TRY(cudaStreamWaitEvent(A->s_h2d, ev0, 0));
+  PJDS_CUDA_TRY(cudaStreamWaitEvent(A->s_d2h, ev0, 0));
+  for (int32_t i = 0; i < count; ++i) {
+    const int b = i & 1;
+    if (!x_host[i] || !y_host[i]) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host_batch: NULL vector");
+    if (i >= 2) PJDS_CUDA_TRY(cudaStreamWaitEvent(A->s_h2d, ev_xf[b], 0));  // product i-2 done reading
+    PJDS_CUDA_TRY(cudaMemcpyAsync(A->d_bx[b], x_host[i], (size_t)A->ncols * vs, cudaMemcpyHostToDevice, A->s_h2d));
+    PJDS_CUDA_TRY(cudaEventRecord(ev_x[b], A->s_h2d));
+    PJDS_CUDA_TRY(cudaStreamWaitEvent(cs, ev_x[b], 0));
+    if (i >= 2) PJDS_CUDA_TRY(cudaStreamWaitEvent(cs, ev_yf[b], 0));  // y of product i-2 copied out
+    if (sym) {
+      PJDS_TRY(launch_permute(A->d_perm, A->h.n, A->d_bx[b], A->d_bp[b], A->h.dtype, 0, cs));
+      PJDS_TRY(launch_pjds_spmv(A, A->d_bx[b], A->d_bp[b], cs, false));  // x slot reused for y_perm
+      PJDS_TRY(launch_permute(A->d_perm, A->h.n, A->d_bx[b], A->d_by[b], A->h.dtype, 1, cs));
+    } else {
+      PJDS_TRY(launch_pjds_spmv(A, A->d_by[b], A->d_bx[b], cs, false));
+    }
+    PJDS_CUDA_TRY(cudaEventRecord(ev_xf[b], cs));
+    PJDS_CUDA_TRY(cudaEventRecord(ev_y[b], cs));
+    PJDS_CUDA_TRY(cudaStreamWaitEvent(A->s_d2h, ev_y[b], 0));
+    PJDS_CUDA_TRY(cudaMemcpyAsync(y_host[i], A->d_by[b], (size_t)A->h.n * vs, cudaMemcpyDeviceToHost, A->s_d2h));
+    PJDS_CUDA_TRY(cudaEventRecord(ev_yf[b], A->s_d2h));
+  }
+  PJDS_CUDA_TRY(cudaEventRecord(ev0, A->s_d2h));
+  PJDS_CUDA_TRY(cudaStreamWaitEvent(cs, ev0, 0));
+  PJDS_CUDA_TRY(cudaStreamSynchronize(cs));
   return PJDS_OK;
 }
 

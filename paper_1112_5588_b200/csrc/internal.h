@@ -73,6 +73,12 @@ struct pjds_mat {
   int32_t* d_perm = nullptr;  // store target per sorted row (orig row; or local row for A_nl)
   void* d_xs = nullptr;       // staging for pjds_spmv_host
   void* d_ys = nullptr;
+  // pipelined host batch (pjds_spmv_host_batch): double-buffered staging, copy streams, events
+  void* d_bx[2] = {nullptr, nullptr};
+  void* d_by[2] = {nullptr, nullptr};
+  void* d_bp[2] = {nullptr, nullptr};  // permuted-basis scratch (x then y) per slot
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_b[9] = {};            // x ready[2], y ready[2], x free[2], y free[2], start
   int64_t ncols = 0;
   bool direct_store = false;  // permuted basis: y[k] stored contiguously, perm not read
   int32_t* d_order[3] = {nullptr, nullptr, nullptr};  // CTA tile execution orders (R = 1, 2, 4)

@@ -298,3 +298,15 @@ def test_tile_order_bitwise(pj, order):
                 check_y(y, n, rp, col, val, x)
     finally:
         L.pjds_set_tile_order(2)
+
+
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_spmv_host_batch_pipelined(pj, symmetric):
+    """Pipelined host-buffer products (double-buffered staging, copy streams) equal the oracle."""
+    n, rp, col, val = inputs.config_crs("C1")
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=symmetric)
+    xs = [torch.from_numpy(inputs.vector(n, seed=100 + i)).pin_memory().numpy() for i in range(5)]
+    ys = [torch.full((n,), float("nan"), dtype=torch.float64).pin_memory().numpy() for _ in range(5)]
+    A.spmv_host_batch(ys, xs)
+    for x, y in zip(xs, ys):
+        check_y(y, n, rp, col, val, x)
