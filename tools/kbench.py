@@ -50,6 +50,7 @@ for cfg in a.configs.split(","):
                                          sigma=int(sg))
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
+          pj.bw_probe(1 << 30, 20)  # host-side conversion leaves the GPU idle: re-raise clocks
           for var, polk, order in [(v, q, o) for v in a.variants.split(",") for q in a.policies.split(",") for o in a.orders.split(",")]:
             pj.lib().pjds_set_tile_order(int(order))
             vr, vu = map(int, var.split("x"))
