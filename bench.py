@@ -63,7 +63,7 @@ def parse():
     p.add_argument("--no-overlap", action="store_true", help="dist: vector mode (exchange, then compute)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-compare", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=30)
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
     p.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
@@ -369,6 +369,26 @@ def main():
                "mode": f"pjds_spmv_host_batch of {a.e2e_steps} products, pinned host buffers, original basis",
                "unpipelined": {"value": round(2.0 * nnz / te / 1e9, 2), "ms_per_step": round(te * 1e3, 3),
                                "mode": "pjds_spmv_host per step (H2D, basis change, kernel, basis change, D2H)"}}
+        # the bound of the pipelined leg: x in and y out at once on two streams, same pinned buffers
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        dx_, dy_ = torch.empty(n, dtype=tdt, device=dev), torch.empty(n, dtype=tdt, device=dev)
+        hx_, hy_ = torch.from_numpy(xh), torch.from_numpy(yh)
+
+        def duplex():
+            s_in.wait_stream(torch.cuda.current_stream())
+            s_out.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_in):
+                dx_.copy_(hx_, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                hy_.copy_(dy_, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s_in)
+            torch.cuda.current_stream().wait_stream(s_out)
+
+        duplex()
+        tp = timed(duplex, 10) * 1e-3
+        e2e["pcie_duplex_ms"] = round(tp * 1e3, 3)
+        e2e["frac_of_pcie_duplex"] = round(tp / tb, 3)
+        del dx_, dy_
         # the paper's PCIe model (Eq. 2-4) with this box's measured bandwidths:
         # B_PCI from the e2e transfer time, B_GPU = the read probe
         t_pci_meas = max(te - t_s, 1e-9)
