@@ -145,6 +145,32 @@ typedef struct {
 
 int pjds_info(pjds_t A, pjds_info_t* out);
 
+/*
+ * Footprint and statistics under the names of SURVEY §8(b) (views of pjds_info / ellr_info):
+ * pjds_footprint — bytes per component (Table 1 L291 and L284-286): values (stored x s_v),
+ *   int32 column indices, col_start (int64, width+1 per window, + window tables), block_len
+ *   (int32, n_blocks), perm (int32, n); bytes_rowmax = 0.  ellr_footprint — values, indices,
+ *   rowmax (int32, N_pad); the pJDS aux fields are 0.  Both: stored / nnz / n_pad entries.
+ * pjds_stats — shape and Fig. 2 counters: n, nnz, n_pad, n_blocks,
+ *   padding = stored - nnz, width, block_rows, row-length min/max/mean, entries-based reduction
+ *   vs ELLPACK (1 - stored / (ceil(n/32)*32 * width)), useful / padded / idle lane-slots.
+ * Host-side only (no device access); INVALID_ARG on NULL.
+ */
+typedef struct {
+  int64_t bytes_values, bytes_indices;
+  int64_t bytes_col_start, bytes_block_len, bytes_perm; /* pJDS aux; 0 for ELLPACK-R */
+  int64_t bytes_rowmax;                                 /* ELLPACK-R aux; 0 for pJDS */
+  int64_t bytes_total, stored, nnz, n_pad;
+} pjds_footprint_t;
+int pjds_footprint(pjds_t A, pjds_footprint_t* out);
+typedef struct {
+  int64_t n, nnz, n_pad, n_blocks, padding;
+  int32_t width, block_rows, len_min, len_max;
+  double len_mean, reduction_vs_ellpack;
+  int64_t useful_fma, padded_fma, idle_lane_slots;
+} pjds_stats_t;
+int pjds_stats(pjds_t A, pjds_stats_t* out);
+
 /* Window layout (host buffers of n_windows+1 entries): wstart[w] = first stored slot of window w
    (wstart[n_windows] = stored); wcs_off[w] = start of window w's col_start in the export array. */
 int pjds_export_windows(pjds_t A, int64_t* wstart, int64_t* wcs_off);
@@ -179,6 +205,7 @@ typedef struct {
   int32_t on_device, device;
 } ellr_info_t;
 int ellr_info(ellr_t A, ellr_info_t* out);
+int ellr_footprint(ellr_t A, pjds_footprint_t* out); /* see pjds_footprint */
 int ellr_export(ellr_t A, int32_t* rowmax, int32_t* col, void* val);
 
 /* ------------------------------------------------------------------ distributed (§3) */
@@ -269,6 +296,11 @@ typedef struct {
   int32_t permuted;
 } pjds_dist_info_t;
 int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* out);
+/* pjds_dist_stats (SURVEY §8(b) name): pjds_dist_info plus the halo size per peer (PAPER.md
+   L442-447): recv_per_peer[q] = entries received from rank q (halo slots owned by q),
+   send_per_peer[q] = entries sent to rank q; caller host arrays of nranks entries, either may be
+   NULL (out may be NULL too).  Sum over q equals halo / send_total. */
+int pjds_dist_stats(pjds_dist_t D, pjds_dist_info_t* out, int64_t* recv_per_peer, int64_t* send_per_peer);
 /* Phase timeline of the last pjds_dist_spmv call made with PJDS_TRACE (CUDA events on the compute
    and comm streams; synchronises them): ms[0] total, [1] start -> local part done, [2] pack,
    [3] NCCL exchange, [4] compute stream waiting for the exchange, [5] nonlocal part.

@@ -145,6 +145,18 @@ class PjdsMatrix:
              beta.ctypes.data, ctypes.byref(steps), _stream_ptr(stream))
         return alpha, beta, steps.value
 
+    def footprint(self) -> dict:
+        """Bytes per component (pjds_footprint: values, indices, col_start, block_len, perm)."""
+        f = _lib.Footprint()
+        call("pjds_footprint", self._h, ctypes.byref(f))
+        return struct_dict(f)
+
+    def stats(self) -> dict:
+        """Shape, padding, row lengths, reduction vs ELLPACK and Fig. 2 counters (pjds_stats)."""
+        st = _lib.Stats()
+        call("pjds_stats", self._h, ctypes.byref(st))
+        return struct_dict(st)
+
     def histogram(self):
         counts = np.zeros(self.info["len_max"] + 1, dtype=np.int64)
         call("pjds_histogram", self._h, counts.ctypes.data, len(counts))
@@ -196,6 +208,12 @@ class EllrMatrix:
         call("ellr_spmv", self._h, _check_vec(y, self.n, self.dtype, "y"), _check_vec(x, self.n, self.dtype, "x"),
              _stream_ptr(stream))
         return y
+
+    def footprint(self) -> dict:
+        """Bytes per component (ellr_footprint: values, indices, rowmax)."""
+        f = _lib.Footprint()
+        call("ellr_footprint", self._h, ctypes.byref(f))
+        return struct_dict(f)
 
     def export(self):
         i = self.info
@@ -391,6 +409,16 @@ class DistPjds:
         call("pjds_dist_permute", self._h, _check_vec(dst, self.n_loc, self.dtype, "dst"),
              _check_vec(src, self.n_loc, self.dtype, "src"), 1, _stream_ptr(stream))
         return dst
+
+    def stats(self) -> dict:
+        """pjds_dist_stats: the dist info plus entries received from / sent to each peer."""
+        inf = _lib.DistInfo()
+        recv = np.zeros(self.nranks, np.int64)
+        send = np.zeros(self.nranks, np.int64)
+        call("pjds_dist_stats", self._h, ctypes.byref(inf), recv.ctypes.data, send.ctypes.data)
+        d = struct_dict(inf)
+        d["recv_per_peer"], d["send_per_peer"] = recv.tolist(), send.tolist()
+        return d
 
     def parts(self):
         a, b = ctypes.c_void_p(), ctypes.c_void_p()

@@ -35,6 +35,19 @@ class EllrInfo(ctypes.Structure):
                 ("on_device", c_i32), ("device", c_i32)]
 
 
+class Footprint(ctypes.Structure):
+    _fields_ = [("bytes_values", c_i64), ("bytes_indices", c_i64), ("bytes_col_start", c_i64),
+                ("bytes_block_len", c_i64), ("bytes_perm", c_i64), ("bytes_rowmax", c_i64),
+                ("bytes_total", c_i64), ("stored", c_i64), ("nnz", c_i64), ("n_pad", c_i64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("nnz", c_i64), ("n_pad", c_i64), ("n_blocks", c_i64), ("padding", c_i64),
+                ("width", c_i32), ("block_rows", c_i32), ("len_min", c_i32), ("len_max", c_i32),
+                ("len_mean", c_dbl), ("reduction_vs_ellpack", c_dbl),
+                ("useful_fma", c_i64), ("padded_fma", c_i64), ("idle_lane_slots", c_i64)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("n_loc", c_i64), ("nnz_loc", c_i64), ("nnz_local_part", c_i64), ("nnz_nonlocal_part", c_i64),
                 ("rows_nonlocal", c_i64), ("halo", c_i64), ("nranks", c_i32), ("rank", c_i32)]
@@ -62,6 +75,9 @@ _SIGS = {
     "pjds_permute": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_info": [c_p, c_p],
     "pjds_histogram": [c_p, c_p, c_i32],
+    "pjds_footprint": [c_p, c_p],
+    "pjds_stats": [c_p, c_p],
+    "ellr_footprint": [c_p, c_p],
     "pjds_export": [c_p, c_p, c_p, c_p, c_p, c_p],
     "ellr_create_from_crs": [c_p, c_i64, c_p, c_p, c_p, ctypes.c_int, c_u32],
     "ellr_destroy": [c_p],
@@ -77,6 +93,7 @@ _SIGS = {
     "pjds_dist_spmv": [c_p, c_p, c_p, c_p, c_u32],
     "pjds_dist_group_spmv": [c_p, c_i32, c_p, c_p, c_p, c_u32],
     "pjds_dist_info": [c_p, c_p],
+    "pjds_dist_stats": [c_p, c_p, c_p, c_p],
     "pjds_dist_trace": [c_p, c_p],
     "pjds_dist_p2p_export": [c_p, c_p, c_p],
     "pjds_dist_p2p_connect": [c_p, c_p, c_i64],

@@ -357,6 +357,44 @@ int ellr_info(ellr_t A, ellr_info_t* o) {
   return PJDS_OK;
 }
 
+int pjds_footprint(pjds_t A, pjds_footprint_t* o) {
+  if (!A || !o) return set_error(PJDS_ERR_INVALID_ARG, "pjds_footprint: NULL argument");
+  const auto& h = A->h;
+  std::memset(o, 0, sizeof(*o));
+  o->bytes_values = h.stored * (int64_t)dtype_size(h.dtype);
+  o->bytes_indices = h.stored * 4;
+  o->bytes_col_start = (int64_t)h.col_start.size() * 8 + (h.n_windows > 1 ? (h.n_windows + 1) * 16 : 0);
+  o->bytes_block_len = h.n_blocks * 4;
+  o->bytes_perm = h.n * 4;
+  o->bytes_total = o->bytes_values + o->bytes_indices + o->bytes_col_start + o->bytes_block_len + o->bytes_perm;
+  o->stored = h.stored; o->nnz = h.nnz; o->n_pad = h.n_pad;
+  return PJDS_OK;
+}
+
+int pjds_stats(pjds_t A, pjds_stats_t* o) {
+  if (!A || !o) return set_error(PJDS_ERR_INVALID_ARG, "pjds_stats: NULL argument");
+  pjds_info_t i;
+  PJDS_TRY(pjds_info(A, &i));
+  std::memset(o, 0, sizeof(*o));
+  o->n = i.n; o->nnz = i.nnz; o->n_pad = i.n_pad; o->n_blocks = i.n_blocks; o->padding = i.stored - i.nnz;
+  o->width = i.width; o->block_rows = i.block_rows; o->len_min = i.len_min; o->len_max = i.len_max;
+  o->len_mean = i.len_mean; o->reduction_vs_ellpack = i.data_reduction_vs_ellpack;
+  o->useful_fma = i.useful_fma; o->padded_fma = i.padded_fma; o->idle_lane_slots = i.idle_lane_slots;
+  return PJDS_OK;
+}
+
+int ellr_footprint(ellr_t A, pjds_footprint_t* o) {
+  if (!A || !o) return set_error(PJDS_ERR_INVALID_ARG, "ellr_footprint: NULL argument");
+  const auto& h = A->h;
+  std::memset(o, 0, sizeof(*o));
+  o->bytes_values = h.stored * (int64_t)dtype_size(h.dtype);
+  o->bytes_indices = h.stored * 4;
+  o->bytes_rowmax = h.n_pad * 4;
+  o->bytes_total = o->bytes_values + o->bytes_indices + o->bytes_rowmax;
+  o->stored = h.stored; o->nnz = h.nnz; o->n_pad = h.n_pad;
+  return PJDS_OK;
+}
+
 int ellr_export(ellr_t A, int32_t* rowmax, int32_t* col, void* val) {
   if (!A) return set_error(PJDS_ERR_INVALID_ARG, "ellr_export: NULL handle");
   const auto& h = A->h;

@@ -606,6 +606,22 @@ int pjds_dist_info(pjds_dist_t D, pjds_dist_info_t* o) {
   return PJDS_OK;
 }
 
+int pjds_dist_stats(pjds_dist_t D, pjds_dist_info_t* o, int64_t* recv_per_peer, int64_t* send_per_peer) {
+  if (!D) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_stats: NULL handle");
+  if (o) PJDS_TRY(pjds_dist_info(D, o));
+  if (recv_per_peer) {
+    for (int q = 0; q < D->R; ++q) recv_per_peer[q] = 0;
+    for (const auto& r : D->recvs)
+      for (const auto& run : r.runs) recv_per_peer[r.peer] += run.second;
+  }
+  if (send_per_peer) {
+    for (int q = 0; q < D->R; ++q) send_per_peer[q] = 0;
+    for (const auto& sd : D->sends)
+      for (const auto& run : sd.runs) send_per_peer[sd.peer] += run.second;
+  }
+  return PJDS_OK;
+}
+
 int pjds_dist_permute(pjds_dist_t D, void* dst, const void* src, int32_t direction, void* stream) {
   if (!D) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_permute: NULL handle");
   return pjds_permute(D->A_loc, dst, src, direction, stream);

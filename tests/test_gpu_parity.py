@@ -184,9 +184,16 @@ def test_dist_group_random(pj, R, permuted):
         ys = [h.from_permuted(torch.empty_like(v), v) for h, v in zip(hs, ys)]
     torch.cuda.synchronize()
     y = np.concatenate([t.cpu().numpy() for t in ys])
-    ref = odist.spmv(odist.split(n, rp, col, val, offs), x)
+    parts = odist.split(n, rp, col, val, offs)
+    ref = odist.spmv(parts, x)
     assert np.array_equal(y, ref)
     check_y(y, n, rp, col, val, x, exact=(R == 1))
+    # pjds_dist_stats: per-peer halo sizes equal the emulator's recv / send lists
+    for r, h in enumerate(hs):
+        st = h.stats()
+        assert st["recv_per_peer"] == [len(v) for v in parts[r]["recv"]]
+        assert st["send_per_peer"] == [len(v) for v in parts[r]["send"]]
+        assert sum(st["recv_per_peer"]) == st["halo"] and sum(st["send_per_peer"]) == st["send_total"]
 
 
 @pytest.mark.parametrize("name,R,permuted", [("C1", 4, False), ("C1", 4, True), ("C3", 4, False), ("C3", 8, True)])

@@ -104,6 +104,40 @@ def test_ellr_conversion_bit_exact(pj, kind, n, kw):
     assert i["bytes_total"] == fp["bytes_total"]
 
 
+@pytest.mark.parametrize("kind,n,kw", CASES[:5])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_footprint_and_stats_entry_points(pj, kind, n, kw, dtype):
+    """pjds_footprint / pjds_stats / ellr_footprint (SURVEY §8(b) names) against the oracle's
+    accounting (oracle/convert.py footprint + utilisation)."""
+    _, rp, col, val = inputs.small(kind, n, seed=5, dtype=dtype, **kw)
+    sv = np.dtype(dtype).itemsize
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=64, host_only=True)
+    P = convert.pjds_reference(n, rp, col, val, b_r=64)
+    ref = convert.footprint(P, value_bytes=sv)["pjds"]
+    f = A.footprint()
+    assert (f["bytes_values"], f["bytes_indices"], f["bytes_total"]) == \
+        (ref["bytes_values"], ref["bytes_indices"], ref["bytes_total"])
+    assert (f["bytes_col_start"], f["bytes_block_len"], f["bytes_perm"], f["bytes_rowmax"]) == \
+        ((P["width"] + 1) * 8, P["n_blocks"] * 4, n * 4, 0)
+    assert (f["stored"], f["nnz"], f["n_pad"]) == (P["stored"], len(col), P["n_pad"])
+    st = A.stats()
+    lens = np.diff(rp)
+    u = convert.utilisation(P, nnz=len(col))["pjds"]
+    assert (st["n"], st["nnz"], st["n_pad"], st["n_blocks"], st["padding"], st["width"], st["block_rows"]) == \
+        (n, len(col), P["n_pad"], P["n_blocks"], P["stored"] - len(col), P["width"], 64)
+    assert (st["len_min"], st["len_max"]) == (int(lens.min()), int(lens.max()))
+    assert st["len_mean"] == pytest.approx(lens.mean(), rel=1e-15)
+    assert st["reduction_vs_ellpack"] == pytest.approx(ref["data_reduction_vs_ellpack"], abs=1e-15)
+    assert (st["useful_fma"], st["padded_fma"], st["idle_lane_slots"]) == (u["useful"], u["padded"], u["idle"])
+    E = pj.EllrMatrix.from_crs(n, rp, col, val, host_only=True)
+    R = convert.ellr_reference(n, rp, col, val)
+    fe = E.footprint()
+    refe = convert.footprint(E=R, value_bytes=sv)["ellr"]
+    assert (fe["bytes_values"], fe["bytes_indices"], fe["bytes_rowmax"], fe["bytes_total"]) == \
+        (refe["bytes_values"], refe["bytes_indices"], refe["bytes_aux"], refe["bytes_total"])
+    assert (fe["bytes_col_start"], fe["bytes_block_len"], fe["bytes_perm"]) == (0, 0, 0)
+
+
 def test_adversarial_closed_form_in_library(pj):
     n = 1024
     _, rp, col, val = inputs.small("adversarial", n, seed=2)
