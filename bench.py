@@ -59,7 +59,7 @@ def parse():
     p.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     p.add_argument("--basis", default="permuted", choices=["permuted", "rows"])
-    p.add_argument("--block-rows", type=int, default=32)
+    p.add_argument("--block-rows", type=int, default=32, help="pJDS b_r (the paper's warp size; 128 = rows per warp at R=4)")
     p.add_argument("--no-overlap", action="store_true", help="dist: vector mode (exchange, then compute)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-compare", action="store_true")
@@ -149,11 +149,11 @@ def _allreduce(dist, t, op):
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
-def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1):
-    """The oracle's plain CRS loop (oracle_spmv_crs: OpenMP static over rows, all visible cores),
-    repeated until the time budget is spent.  Returns (median seconds per product, reps, cores)."""
+def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1, threads: int = 0):
+    """The oracle's plain CRS loop (oracle_spmv_crs: OpenMP static over rows, all visible cores or
+    `threads`), repeated until the time budget is spent.  Returns (median s per product, reps, cores, total s)."""
     import oracle
-    cores = len(os.sched_getaffinity(0))
+    cores = threads or len(os.sched_getaffinity(0))
     oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)  # warm-up
     ts = []
     t_end = time.perf_counter() + budget_s
@@ -242,6 +242,8 @@ def main():
         cpu = {"value": round(2.0 * nnz_loc / t / 1e9, 3), "unit": "GFlop/s", "cores": cores, "kind": "oracle",
                "sample": f"whole {a.config} matrix ({nnz_loc} nnz), {reps} products, median; {tot:.1f} s of "
                          f"oracle_spmv_crs ({np.dtype(npdt).name}, OpenMP {cores} threads)"}
+        t1, reps1, _, _ = time_oracle(n, rp, col, val, x_host, budget_s=3.0, max_reps=3, threads=1)
+        cpu["single_thread"] = {"value": round(2.0 * nnz_loc / t1 / 1e9, 3), "reps": reps1}
     nnz = nnz_loc
     if use_dist:
         tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
@@ -296,6 +298,19 @@ def main():
         lt = torch.tensor([launches], dtype=torch.int64, device=dev)
         _allreduce(dist, lt, "sum")
         launches = int(lt.item())
+    # SURVEY §8(d) protocol beside the contract timing: 5 trials of >= 20 ms of back-to-back steps
+    kt = max(10, int(np.ceil(20.0 / max(ms, 1e-3))))
+    tr = []
+    for _ in range(5):
+        if use_dist:
+            dist.barrier()
+        tr.append(timed(step, kt))
+    if use_dist:
+        tv = torch.tensor(tr, dtype=torch.float64, device=dev)
+        _allreduce(dist, tv, "max")
+        tr = tv.tolist()
+    trials = {"n": 5, "steps_each": kt, "median_ms": round(float(np.median(tr)), 5), "best_ms": round(min(tr), 5),
+              "best_gflops": round(2.0 * nnz / (min(tr) * 1e-3) / 1e9, 2)}
     dist_info = None
     if use_dist:
         # vector mode (exchange, then compute) as the reference point for "communication hidden",
@@ -328,13 +343,19 @@ def main():
     achieved = b_min / t_s / 1e9 / world  # per GPU
     peak = peak_file if peak_file else max(probe_copy, probe_read)
 
+    traffic_key = f"{a.config}/{a.dtype}/{a.basis}" + ("" if a.block_rows == 32 else f"/br{a.block_rows}")
+
     # side-by-side kernels on the same matrix (N=1): rows-only pJDS and ELLPACK-R
     if not use_dist and a.impl == "pjds" and not a.no_compare:
         x0 = torch.from_numpy(x_host).to(dev)
-        for name, mk in (("pjds_rows_only" if permuted else "pjds_permuted",
-                          lambda: pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows,
-                                                         symmetric=not permuted)),
-                         ("ellpack_r", lambda: pj.EllrMatrix.from_crs(n, rp, col, val))):
+        legs = [("pjds_rows_only" if permuted else "pjds_permuted",
+                 lambda: pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows, symmetric=not permuted)),
+                ("ellpack_r", lambda: pj.EllrMatrix.from_crs(n, rp, col, val))]
+        # b_r sweep point: b_r = 32 (paper) vs 128 (= rows one warp owns at R=4)
+        br_alt = 128 if a.block_rows == 32 else 32
+        legs.insert(0, (f"pjds_br{br_alt}", lambda: pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br_alt,
+                                                                           symmetric=permuted)))
+        for name, mk in legs:
             B = mk()
             for _ in range(3):
                 B.spmv(y, x0, stream=stream)
@@ -394,7 +415,7 @@ def main():
         t_pci_meas = max(te - t_s, 1e-9)
         b_pci = 2 * n * sv / t_pci_meas
         ratio = max(probe_copy, probe_read) * 1e9 / b_pci
-        traffic = committed_traffic(f"{a.config}/{a.dtype}/{a.basis}")
+        traffic = committed_traffic(traffic_key)
         alpha = (perfmodel.measured_alpha(traffic - n * sv, A.info["stored"], nnz, n, sv,
                                           aux_bytes=A.info["bytes_aux"] - A.info["n"] * 4 * permuted)
                  if traffic else None)
@@ -452,13 +473,15 @@ def main():
             "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": (committed_traffic(f"{a.config}/{a.dtype}/{a.basis}")
+                         "traffic": (committed_traffic(traffic_key)
                                      if not use_dist and a.impl == "pjds" else None),
                          "traffic_source": "profiles/r01_traffic.json (ncu --set full, per launch)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peak_file else "bw probe (this run)",
                          "probe_copy_gbs": round(probe_copy, 1), "probe_read_gbs": round(probe_read, 1),
                          "frac_of_probe_max": round(achieved / max(probe_copy, probe_read), 4),
+                         "frac_of_nominal_8000": round(achieved / 8000.0, 4),
                          "algorithmic_bytes_per_step": b_min},
+            "trials": trials,
             "e2e": e2e,
             "perf_model": model,
             "gpu_launches": launches,

@@ -22,12 +22,13 @@ lines = ["# Measured RHS re-load factor alpha (x elements read from DRAM per sto
 info = {}
 for (c, t, f), (i, m) in zip(labels, d.items()):
     sv = 8 if t == "f64" else 4
-    if (c, t) not in info:
+    br = int(f[4:].rstrip("s")) if f.startswith("pjds") else 32
+    if (c, t, br) not in info:
         n, rp, col, val = inputs.config_crs(c, dtype=np.float64 if sv == 8 else np.float32)
-        A = pj.PjdsMatrix.from_crs(n, rp, col, val, host_only=True)
+        A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, host_only=True)
         E = pj.EllrMatrix.from_crs(n, rp, col, val, host_only=True)
-        info[(c, t)] = (n, len(col), A.info, E.info)
-    n, nnz, ai, ei = info[(c, t)]
+        info[(c, t, br)] = (n, len(col), A.info, E.info)
+    n, nnz, ai, ei = info[(c, t, br)]
     rd, wr, tns = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"], m["gpu__time_duration.sum"]
     bmin = pm.min_bytes(nnz, n, sv)
     if f.startswith("pjds"):
