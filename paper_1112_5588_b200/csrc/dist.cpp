@@ -385,6 +385,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
     D->A_loc = new pjds_mat();
     s = convert_pjds(D->A_loc->h, P->n_loc, P->n_loc, P->loc_rowptr.data(), P->loc_col.data(), v_loc.data(), dtype,
                      block_rows, sym);
+    if (s != PJDS_OK) return fail(s);  // (perm is not filled on failure)
     // local inverse permutation (permuted basis: local row i lives at position inv[i])
     std::vector<int32_t> inv;
     if (sym) {
@@ -393,8 +394,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       D->A_loc->direct_store = true;
       D->A_loc->flags = PJDS_PERM_SYMMETRIC;
     }
-    if (s == PJDS_OK) s = upload_pjds(D->A_loc, nullptr);
-    if (s != PJDS_OK) return fail(s);
+    if ((s = upload_pjds(D->A_loc, nullptr)) != PJDS_OK) return fail(s);
     D->A_loc->ncols = P->n_loc;
     const int64_t m = (int64_t)P->rows_nl.size();
     if (m > 0) {
