@@ -110,7 +110,8 @@ int pjds_permute(pjds_t A, void* dst, const void* src, int32_t direction, void* 
  * pinned is faster): copies x host->device, (PJDS_PERM_SYMMETRIC: permutes x to the permuted
  * basis), runs the pJDS kernel, (permutes y back), copies y device->host, synchronises `stream`.
  * The transfer cost is the paper's T_PCI (Eq. 2).  Staging buffers are
- * allocated on first use and owned by the handle.
+ * allocated on first use and owned by the handle, so calls on one handle must not run
+ * concurrently from several host threads (pjds_spmv itself has no such restriction).
  */
 int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream);
 
@@ -119,7 +120,8 @@ int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream);
  * (original basis), pipelined: the host->device copy of x_{i+1} and the device->host copy of y_{i-1}
  * run on two copy streams while product i runs on `stream` (double-buffered staging owned by the
  * handle), so PCIe traffic in both directions overlaps the kernels.  Host vectors should be
- * pinned for the copies to be asynchronous.  Synchronises `stream` before returning.
+ * pinned for the copies to be asynchronous.  Synchronises `stream` before returning.  Same
+ * one-caller-at-a-time rule per handle as pjds_spmv_host.
  */
 int pjds_spmv_host_batch(pjds_t A, void* const* y_host, const void* const* x_host, int32_t count,
                          void* stream);

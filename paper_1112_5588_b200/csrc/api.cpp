@@ -15,9 +15,11 @@ int set_error(int status, const std::string& msg) {
 template <typename P>
 static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
   *dst = nullptr;
-  if (bytes == 0) bytes = 16;  // keep a valid pointer for empty arrays
-  PJDS_CUDA_TRY(cudaMalloc((void**)dst, bytes));
-  if (src) PJDS_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  // empty arrays still get a (16-byte, zeroed) allocation so the kernels see a valid pointer;
+  // only the `bytes` that exist on the host are copied
+  PJDS_CUDA_TRY(cudaMalloc((void**)dst, bytes ? bytes : 16));
+  if (!bytes) PJDS_CUDA_TRY(cudaMemset(*dst, 0, 16));
+  if (src && bytes) PJDS_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
   return PJDS_OK;
 }
 
@@ -117,13 +119,9 @@ int pjds_create_from_crs_ex(pjds_t* out, int64_t n, const int64_t* rowptr, const
   A->flags = flags;
   int s = convert_pjds(A->h, n, n, rowptr, col, val, dtype, block_rows, flags & PJDS_PERM_SYMMETRIC, sigma);
   if (s == PJDS_OK && !(flags & PJDS_HOST_ONLY)) {
-    if (flags & PJDS_PERM_SYMMETRIC) {
-      // permuted basis: y_perm[k] is stored at k; the kernel does not read perm at all
-      A->direct_store = true;
-      s = upload_pjds(A, nullptr);
-    } else {
-      s = upload_pjds(A, nullptr);
-    }
+    // permuted basis: y_perm[k] is stored at k; the kernel does not read perm at all
+    A->direct_store = flags & PJDS_PERM_SYMMETRIC;
+    s = upload_pjds(A, nullptr);
   }
   if (s != PJDS_OK) {
     delete A;
@@ -148,9 +146,9 @@ int pjds_destroy(pjds_t A) {
 }
 
 int pjds_spmv(pjds_t A, void* y, const void* x, void* stream) {
-  if (!A || !y || (!x && A->h.n > 0)) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: NULL argument");
+  if (!A || (A->h.n > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: NULL argument");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: handle is host-only");
-  if (y == x) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: y aliases x");
+  if (y == x && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: y aliases x");
   return launch_pjds_spmv(A, y, x, (cudaStream_t)stream, false);
 }
 
@@ -336,9 +334,9 @@ int ellr_destroy(ellr_t A) {
 }
 
 int ellr_spmv(ellr_t A, void* y, const void* x, void* stream) {
-  if (!A || !y || (!x && A->h.n > 0)) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: NULL argument");
+  if (!A || (A->h.n > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: NULL argument");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: handle is host-only");
-  if (y == x) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: y aliases x");
+  if (y == x && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: y aliases x");
   return launch_ellr_spmv(A, y, x, (cudaStream_t)stream);
 }
 

@@ -229,6 +229,25 @@ def test_bw_probe_and_launch_count(pj):
     assert pj.launch_count() > c0
 
 
+def test_empty_matrix(pj):
+    """n = 0 (n = 0 accepted): create, spmv with empty (possibly NULL) vectors, info."""
+    rp = np.zeros(1, np.int64)
+    col = np.zeros(0, np.int32)
+    for dt in (np.float64, np.float32):
+        val = np.zeros(0, dt)
+        tdt = torch.float64 if dt == np.float64 else torch.float32
+        x = torch.empty(0, dtype=tdt, device="cuda")
+        y = torch.empty(0, dtype=tdt, device="cuda")
+        A = pj.PjdsMatrix.from_crs(0, rp, col, val)
+        assert A.info["n"] == 0 and A.info["stored"] == 0
+        A.spmv(y, x)
+        E = pj.EllrMatrix.from_crs(0, rp, col, val)
+        E.spmv(y, x)
+        S = pj.PjdsMatrix.from_crs(0, rp, col, val, symmetric=True)
+        S.spmv(y, x)
+        torch.cuda.synchronize()
+
+
 def test_misuse_errors(pj):
     n, rp, col, val = inputs.config_crs("C1")
     A = pj.PjdsMatrix.from_crs(n, rp, col, val)
