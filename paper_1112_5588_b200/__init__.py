@@ -327,6 +327,8 @@ class DistPjds:
         h = ctypes.c_void_p()
         call("pjds_dist_create", ctypes.byref(h), plan._h, val_loc.ctypes.data, _dt(val_loc), int(block_rows),
              sc.ctypes.data, scols.ctypes.data, tr, uid, PJDS_PERM_SYMMETRIC if permuted else 0)
+        obj = cls(h, plan.info, R, rank, _dt(val_loc))  # owns h from here on (freed on any later error)
+        plan.close()
         if transport == "p2p":
             nb = ctypes.c_int64()
             call("pjds_dist_p2p_export", h, None, ctypes.byref(nb))
@@ -337,9 +339,7 @@ class DistPjds:
             allb = b"".join(blobs)
             call("pjds_dist_p2p_connect", h, ctypes.c_char_p(allb), nb.value)
             dist.barrier(group=group)
-        info = plan.info
-        plan.close()
-        return cls(h, info, R, rank, _dt(val_loc))
+        return obj
 
     def p2p_timed_out(self) -> bool:
         v = ctypes.c_int32()

@@ -63,14 +63,16 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
   }
   // kernel view of col_start: per window w, wstart[w] + col_start_w[j] - w * sigma, so that the
   // slot of sorted row k in column j is cs[j] + k for every window
+  // (n = 0 has no window: its col_start is the single entry {0})
   std::vector<int64_t> cs_abs(h.col_start.size());
-  for (int64_t w = 0; w < std::max<int64_t>(h.n_windows, 1); ++w) {
-    const int64_t a0 = h.wcs_off.empty() ? 0 : h.wcs_off[w];
-    const int64_t a1 = h.wcs_off.empty() ? (int64_t)cs_abs.size() : h.wcs_off[w + 1];
-    const int64_t add = (h.wstart.empty() ? 0 : h.wstart[w]) - w * h.sigma;
+  const bool windowed = h.n_windows >= 1 && (int64_t)h.wcs_off.size() == h.n_windows + 1;
+  for (int64_t w = 0; w < (windowed ? h.n_windows : 1); ++w) {
+    const int64_t a0 = windowed ? h.wcs_off[w] : 0;
+    const int64_t a1 = windowed ? h.wcs_off[w + 1] : (int64_t)cs_abs.size();
+    const int64_t add = (windowed ? h.wstart[w] : 0) - w * h.sigma;
     for (int64_t i = a0; i < a1; ++i) cs_abs[i] = h.col_start[i] + add;
   }
-  std::vector<int64_t> woff = h.wcs_off.empty() ? std::vector<int64_t>{0, (int64_t)cs_abs.size()} : h.wcs_off;
+  std::vector<int64_t> woff = windowed ? h.wcs_off : std::vector<int64_t>{0, (int64_t)cs_abs.size()};
   int s = PJDS_OK;
   if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
       (s = dmalloc_copy(&A->d_col, h.col.data(), h.col.size() * 4)) ||
@@ -231,7 +233,7 @@ int pjds_spmv_host_batch(pjds_t A, void* const* y_host, const void* const* x_hos
 int pjds_permute(pjds_t A, void* dst, const void* src, int32_t direction, void* stream) {
   if (!A || (A->h.n > 0 && (!dst || !src))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: NULL argument");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: handle is host-only");
-  if (dst == src) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: dst aliases src");
+  if (dst == src && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: dst aliases src");
   if (direction != 0 && direction != 1) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: direction 0 or 1");
   return launch_permute(A->d_perm, A->h.n, src, dst, A->h.dtype, direction, (cudaStream_t)stream);
 }

@@ -7,6 +7,14 @@ import torch, torch.distributed as dist
 import inputs, oracle, paper_1112_5588_b200 as pj
 from oracle import dist as odist
 rank = int(os.environ["RANK"]); R = int(os.environ["WORLD_SIZE"])
+
+
+def emit(obj):
+    """One JSON line in a single write(2): the ranks share the parent's stdout pipe, and print()
+    may split a line into several writes that interleave with another rank's."""
+    os.write(1, (json.dumps(obj) + "\n").encode())
+
+
 torch.cuda.set_device(0)
 dist.init_process_group("gloo")
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
@@ -27,7 +35,7 @@ for permuted in (False, True):
         D = pj.DistPjds.create(n, offs, rp[lo:hi + 1] - rp[lo], col[rp[lo]:rp[hi]], val[rp[lo]:rp[hi]],
                                permuted=permuted, transport=transport)
     except Exception as e:
-        print(json.dumps({"rank": rank, "create_error": str(e)[:300]})); sys.exit(0)
+        emit({"rank": rank, "create_error": str(e)[:300]}); sys.exit(0)
     xt = torch.from_numpy(x[lo:hi].copy()).cuda()
     if permuted:
         xt = D.to_permuted(torch.empty_like(xt), xt)
@@ -48,5 +56,5 @@ for permuted in (False, True):
                                                      "trace": D.trace(), "halo": D.info["halo"], "messages": D.info["send_messages"],
                                                      "timed_out": D.p2p_timed_out()}
     D.close()
-print(json.dumps({"rank": rank, **out}))
+emit({"rank": rank, **out})
 dist.destroy_process_group()

@@ -196,6 +196,27 @@ def test_dist_group_random(pj, R, permuted):
         assert sum(st["recv_per_peer"]) == st["halo"] and sum(st["send_per_peer"]) == st["send_total"]
 
 
+@pytest.mark.parametrize("permuted", [False, True])
+def test_dist_group_empty_ranks(pj, permuted):
+    """Ranks owning no rows (repeated offsets) take part with empty local/nonlocal parts."""
+    n = 2000
+    _, rp, col, val = inputs.small("random", n, seed=8, max=40)
+    x = inputs.vector(n)
+    offs = np.array([0, 0, 700, 700, 2000, 2000], np.int64)
+    R = len(offs) - 1
+    hs = pj.DistPjds.create_group(n, rp, col, val, offs, permuted=permuted)
+    xs = [tdev(x[offs[r]:offs[r + 1]]) for r in range(R)]
+    if permuted:
+        xs = [h.to_permuted(torch.empty_like(v), v) for h, v in zip(hs, xs)]
+    ys = [torch.full((int(offs[r + 1] - offs[r]),), float("nan"), dtype=torch.float64, device="cuda") for r in range(R)]
+    pj.DistPjds.group_spmv(hs, ys, xs)
+    if permuted:
+        ys = [h.from_permuted(torch.empty_like(v), v) for h, v in zip(hs, ys)]
+    torch.cuda.synchronize()
+    y = np.concatenate([t.cpu().numpy() for t in ys])
+    assert np.array_equal(y, odist.spmv(odist.split(n, rp, col, val, offs), x))
+
+
 @pytest.mark.parametrize("name,R,permuted", [("C1", 4, False), ("C1", 4, True), ("C3", 4, False), ("C3", 8, True)])
 def test_dist_group_configs(pj, name, R, permuted):
     n, rp, col, val = inputs.config_crs(name)

@@ -184,6 +184,18 @@ def test_dist_plan_matches_oracle(pj, R):
     n = 400
     _, rp, col, val = inputs.small("random", n, seed=10 + R, max=30)
     offs = np.array([n * r // R for r in range(R + 1)], np.int64)
+    _check_plan(pj, n, rp, col, val, offs)
+
+
+def test_dist_plan_empty_ranks(pj):
+    """Ranks that own no rows (offsets repeat) plan an empty local part and receive nothing."""
+    n = 300
+    _, rp, col, val = inputs.small("random", n, seed=4, max=40)
+    _check_plan(pj, n, rp, col, val, np.array([0, 0, 120, 120, 300, 300], np.int64))
+
+
+def _check_plan(pj, n, rp, col, val, offs):
+    R = len(offs) - 1
     ref = odist.split(n, rp, col, val, offs)
     for r in range(R):
         lo, hi = offs[r], offs[r + 1]
