@@ -328,8 +328,9 @@ int pjds_nccl_unique_id(void* out128);
  *   v_0 = v0/||v0||; w = A v_j; alpha_j = w.v_j; w -= alpha_j v_j + beta_{j-1} v_{j-1};
  *   beta_j = ||w||; v_{j+1} = w / beta_j.
  * Precondition: A symmetric (not checked).  v0: device vector (permuted basis, handle dtype, n
- * entries, not modified).  alpha[m], beta[m]: host outputs (double).  *steps_done = m, or j+1 if
- * beta_j = 0 (invariant subspace).  Dot products accumulate in double.  The m iterations (pJDS
+ * entries, not modified; INVALID_ARG if its norm is 0).  alpha[m], beta[m]: host outputs (double).
+ * *steps_done = m, or j+1 if beta_j = 0 exactly (invariant subspace; entries past steps_done are
+ * unspecified).  Dot products accumulate in double.  The m iterations (pJDS
  * kernel + 2 fused vector passes + 2 one-CTA reductions each) are captured into one CUDA graph and
  * launched on `stream`; the call synchronises `stream`.  Work buffers (3 vectors) are allocated
  * and freed inside.

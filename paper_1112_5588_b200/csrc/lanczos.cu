@@ -183,6 +183,10 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
   LZ_TRY(cudaMemcpyAsync(h.data(), scal, h.size() * sizeof(double), cudaMemcpyDeviceToHost, user));
   LZ_TRY(cudaStreamSynchronize(user));
 #undef LZ_TRY
+  if (!(h[0] > 0.0)) {  // scal[0] = 1/||v0||, 0 when v0 = 0 (or non-finite)
+    cleanup();
+    return set_error(PJDS_ERR_INVALID_ARG, "pjds_lanczos: v0 has zero (or non-finite) norm");
+  }
   int done = m;
   for (int j = 0; j < m; ++j) {
     alpha[j] = h[(m + 1) + j];

@@ -45,7 +45,8 @@ def check_y(y_gpu, n, rp, col, val, x, exact=True):
 
 SMALL = [("uniform", 1000, {}), ("clustered", 777, {}), ("empty_rows", 513, {}), ("duplicates", 300, {}),
          ("random", 1500, dict(max=90)), ("adversarial", 1024, {}), ("constant", 96, dict(k=7)), ("zero", 70, {}),
-         ("identity", 31, {}), ("banded", 2049, {})]
+         ("identity", 31, {}), ("banded", 2049, {}),
+         ("adversarial", 3000, {})]  # width 3000 > the 1024 col_start entries staged in shared memory
 
 
 @pytest.mark.parametrize("kind,n,kw", SMALL)

@@ -95,3 +95,27 @@ def test_gpu_lanczos_matches_oracle(dtype):
         assert np.abs(b[:10] - rb[:10]).max() <= tol * scale, name
         ev, rv = pj.tridiag_eigenvalues(a, b), olz.ritz_values(ra, rb)
         assert abs(ev[0] - rv[0]) <= 10 * tol * scale and abs(ev[-1] - rv[-1]) <= 10 * tol * scale, name
+
+
+@pytest.mark.gpu
+def test_gpu_lanczos_breakdown_and_zero_start():
+    """A = 2 I with v0 = e_0: alpha_0 = 2 and w = 0 exactly, so the recurrence stops after one step
+    (steps_done = 1), as the oracle does; a zero start vector is rejected."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    import paper_1112_5588_b200 as pj
+    n = 500
+    rp = np.arange(n + 1, dtype=np.int64)
+    col = np.arange(n, dtype=np.int32)
+    val = np.full(n, 2.0)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+    perm = A.export()["perm"]
+    e0 = np.zeros(n)
+    e0[0] = 1.0
+    a, b, steps = A.lanczos(torch.from_numpy(e0[perm].copy()).cuda(), 10)
+    ra, rb = olz.lanczos(n, rp, col, val, e0, 10)
+    assert steps == 1 == len(ra)
+    assert a[0] == ra[0] == 2.0 and b[0] == rb[0] == 0.0
+    with pytest.raises(pj.PjdsError):
+        A.lanczos(torch.zeros(n, dtype=torch.float64, device="cuda"), 5)
