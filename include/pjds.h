@@ -355,7 +355,11 @@ int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gb
    variant computes bit-identical y (one FMA chain per row, stored order).  unroll + 16 selects
    the software-pipelined main loop (next chunk's loads issued before the current FMAs);
    rows_per_thread + 8 forces the 64-bit jagged-offset kernels (used when stored + n_pad >= 2^31)
-   on any matrix, so tests can cover them. */
+   on any matrix, so tests can cover them.  rows_per_thread = 16 + S selects the long-row split-j
+   kernel (S in {2,4} with unroll 4 or 8, or S = 8 with unroll 4): S warps share 32 rows, each
+   runs the chain over slots j = s mod S, partials added in the tree ((p0+p1)+(p2+p3))+... — a
+   different (fixed, deterministic) summation order from the single chain, within the same O2
+   bound. */
 int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
 
 /* Tuning knob (process-wide): L2 eviction priority of the pJDS kernel's streamed val/col loads

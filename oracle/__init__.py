@@ -38,6 +38,7 @@ def _load():
         P = ctypes.c_void_p
         lib.oracle_spmv_ld.argtypes = [ctypes.c_int64, P, P, P, P, ctypes.c_int, P, P]
         lib.oracle_spmv_chain.argtypes = [ctypes.c_int64, P, P, P, P, ctypes.c_int, P]
+        lib.oracle_spmv_split_chain.argtypes = [ctypes.c_int64, P, P, P, P, ctypes.c_int, ctypes.c_int, P]
         lib.oracle_spmv_crs.argtypes = [ctypes.c_int64, P, P, P, P, ctypes.c_int, P, ctypes.c_int]
         lib.oracle_max_threads.restype = ctypes.c_int
         _lib = lib
@@ -74,6 +75,17 @@ def spmv_chain(n, rowptr, col, val, x):
     y = np.empty(n, dtype=val.dtype)
     _load().oracle_spmv_chain(n, rowptr.ctypes.data, col.ctypes.data, val.ctypes.data, x.ctypes.data, dt,
                               y.ctypes.data)
+    return y
+
+
+def spmv_split_chain(n, rowptr, col, val, x, S: int):
+    """Split-j arithmetic: S interleaved FMA chains per row (entries j = s mod S, CRS order, from +0)
+    combined by the pairwise tree ((p0+p1)+(p2+p3))+...; S = 1 is spmv_chain (see oracle.c)."""
+    assert S >= 1 and S & (S - 1) == 0 and S <= 64
+    rowptr, col, val, x, dt = _prep(n, rowptr, col, val, x)
+    y = np.empty(n, dtype=val.dtype)
+    _load().oracle_spmv_split_chain(n, rowptr.ctypes.data, col.ctypes.data, val.ctypes.data, x.ctypes.data, dt,
+                                    int(S), y.ctypes.data)
     return y
 
 

@@ -68,6 +68,40 @@ void oracle_spmv_chain(int64_t n, const int64_t* rowptr, const int32_t* col, con
   }
 }
 
+/* The long-row ("split-j") kernel variant's arithmetic (SURVEY §8(c) O3 exemption for split-j
+ * kernels; NEXT-4): for S threads per row, partial p_s = fma chain from +0.0 over the row's stored
+ * entries with position j = s, s+S, s+2S, ... (CRS order), then the pairwise tree
+ * ((p_0+p_1)+(p_2+p_3))+... over s = 0..S-1 (S a power of two).  S = 1 is oracle_spmv_chain. */
+void oracle_spmv_split_chain(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                             const void* x, int dtype, int S, void* y) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double pd[64];
+    float pf[64];
+    const int64_t r0 = rowptr[i], len = rowptr[i + 1] - rowptr[i];
+    for (int s = 0; s < S; ++s) {
+      if (dtype == 1) {
+        double acc = 0.0;
+        for (int64_t j = s; j < len; j += S)
+          acc = fma(((const double*)val)[r0 + j], ((const double*)x)[col[r0 + j]], acc);
+        pd[s] = acc;
+      } else {
+        float acc = 0.0f;
+        for (int64_t j = s; j < len; j += S)
+          acc = fmaf(((const float*)val)[r0 + j], ((const float*)x)[col[r0 + j]], acc);
+        pf[s] = acc;
+      }
+    }
+    for (int w = 1; w < S; w *= 2)  /* level w: p_s += p_{s+w} for s a multiple of 2w */
+      for (int s = 0; s + w < S; s += 2 * w) {
+        if (dtype == 1) pd[s] = pd[s] + pd[s + w];
+        else pf[s] = pf[s] + pf[s + w];
+      }
+    if (dtype == 1) ((double*)y)[i] = pd[0];
+    else ((float*)y)[i] = pf[0];
+  }
+}
+
 void oracle_spmv_crs(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
                      const void* x, int dtype, void* y, int nthreads) {
   if (nthreads > 0) omp_set_num_threads(nthreads);

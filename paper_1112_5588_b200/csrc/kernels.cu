@@ -298,6 +298,98 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   }
 }
 
+// Long-row ("split-j") variant: S warps share one group of 32 rows so that long
+// rows (DLR1/DLR2/UHBR, N_nzr 123-315) do not leave each thread a long serial chain of dependent
+// gathers.  Warp w of a CTA works on row group w / S as sub s = w % S: lane l owns row
+// cta_k0 + 32*(w / S) + l and runs the FMA chain over its slots j = s, s+S, s+2S, ... < block_len
+// from +0 (every load instruction still reads 32 consecutive slots of one jagged column); the S
+// partial sums meet in shared memory and sub 0 adds them in the fixed tree ((p0+p1)+(p2+p3))+...
+// Not the single-chain order of reading 14: checked bitwise against oracle_spmv_split_chain and
+// against the O2 bound.
+template <typename T, typename Off, int S, int U, int MODE>
+__global__ void __launch_bounds__(kThreads)
+pjds_spmv_split_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
+                       const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
+                       T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, double* __restrict__ dot_part,
+                       int64_t sigma, const int64_t* __restrict__ wcs_off) {
+  constexpr int kWarps = kThreads / 32;
+  constexpr int RPC = 32 * kWarps / S;  // rows per CTA
+  __shared__ Off s_cs[kSmemCS];
+  __shared__ T s_part[kWarps][32];
+  const int64_t cta_k0 = (int64_t)blockIdx.x * RPC;
+  const int cta_len = block_len[cta_k0 / br];
+  col_start += wcs_off[cta_k0 / sigma];
+  const int lim = min(cta_len + 1, kSmemCS);
+  for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int sub = w % S;
+  const int64_t k = cta_k0 + 32 * (w / S) + lane;
+  const bool active = k < n_pad;
+  T acc = T(0);
+  if (active) {
+    const int len = block_len[k / br];  // 32 rows of a group share one block (b_r % 32 == 0)
+    const uint64_t pol_s = make_policy(pol & 0xff);
+    const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
+    auto cs = [&](int j) -> Off { return j < kSmemCS ? s_cs[j] : (Off)col_start[j]; };
+    int j = sub;
+    for (; j + S * (U - 1) < len; j += S * U) {
+      T v[U];
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const Off o = cs(j + S * u) + (Off)k;
+        v[u] = ld_stream(val + o, pol_s);
+        c[u] = ld_stream(col + o, pol_s);
+      }
+      T xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_rhs(x + c[u], pol_x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = fma_rn(v[u], xv[u], acc);
+    }
+    for (; j < len; j += S) {
+      const Off o = cs(j) + (Off)k;
+      acc = fma_rn(ld_stream(val + o, pol_s), ld_rhs(x + ld_stream(col + o, pol_s), pol_x), acc);
+    }
+  }
+  s_part[w][lane] = acc;
+  __syncthreads();
+  const bool owner = active && sub == 0 && k < n;
+  if (sub == 0) {
+    // pairwise tree over the group's S partials (warps w .. w+S-1)
+    T p[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) p[q] = s_part[w + q][lane];
+#pragma unroll
+    for (int step = 1; step < S; step *= 2)
+#pragma unroll
+      for (int q = 0; q + step < S; q += 2 * step) p[q] = p[q] + p[q + step];
+    acc = p[0];
+    if (owner) {
+      if (MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) {
+        y[k] = acc;
+      } else {
+        const int pr = perm[k];
+        if (MODE == STORE_PERM_ACC) y[pr] = y[pr] + acc;
+        else y[pr] = acc;
+      }
+    }
+  }
+  if (MODE == STORE_DIRECT_DOT) {
+    __shared__ double s_red[kWarps];
+    double d = owner ? (double)acc * (double)x[k] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane == 0) s_red[w] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tsum = 0.0;
+      for (int q = 0; q < kWarps; ++q) tsum += s_red[q];
+      dot_part[blockIdx.x] = tsum;
+    }
+  }
+}
+
 static int g_pol = 1 | (2 << 8);  // val/col evict_first, x evict_last
 static int g_tile_order = 2;  // 0 storage order, 1 by first row's original index, 2 auto (see launch_pjds_t)
 
@@ -356,14 +448,45 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   return PJDS_OK;
 }
 
+template <typename T, typename Off, int S, int U>
+int launch_pjds_split_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part,
+                        int64_t* nparts) {
+  const auto& h = A->h;
+  const int64_t grid = (h.n_pad * S + kThreads - 1) / kThreads;
+  if (nparts) *nparts = grid;
+  if (grid == 0) return PJDS_OK;
+#define PJDS_LAUNCH_SPLIT(M)                                                                            \
+  pjds_spmv_split_kernel<T, Off, S, U, M><<<(unsigned)grid, kThreads, 0, s>>>(                           \
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, \
+      dot_part, h.sigma, A->d_wcs_off)
+  if (mode == STORE_DIRECT) PJDS_LAUNCH_SPLIT(STORE_DIRECT);
+  else if (mode == STORE_DIRECT_DOT) PJDS_LAUNCH_SPLIT(STORE_DIRECT_DOT);
+  else if (mode == STORE_PERM_ACC) PJDS_LAUNCH_SPLIT(STORE_PERM_ACC);
+  else PJDS_LAUNCH_SPLIT(STORE_PERM);
+#undef PJDS_LAUNCH_SPLIT
+  count_launch();
+  PJDS_CUDA_TRY(cudaGetLastError());
+  return PJDS_OK;
+}
+
 // kernel variant (rows per thread R, j-unroll U); 0 = automatic choice
 static int g_var_r = 0, g_var_u = 0;
+static int g_split = 0;  // > 0: long-row variant with S = g_split threads per row (knob rows_per_thread = 16 + S)
 static bool g_force_off64 = false;  // test hook: exercise the 64-bit offset kernels on small inputs
 
 template <typename T, typename Off>
 int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode, double* dp, int64_t* np) {
   int R = g_var_r, U = g_var_u;
   bool pipe = g_pipe;
+  if (g_split) {
+    T* yy = (T*)y;
+    const T* xx = (const T*)x;
+    if (g_split == 2) return U >= 8 ? launch_pjds_split_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np)
+                                    : launch_pjds_split_t<T, Off, 2, 4>(A, yy, xx, s, mode, dp, np);
+    if (g_split == 4) return U >= 8 ? launch_pjds_split_t<T, Off, 4, 8>(A, yy, xx, s, mode, dp, np)
+                                    : launch_pjds_split_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np);
+    return launch_pjds_split_t<T, Off, 8, 4>(A, yy, xx, s, mode, dp, np);
+  }
   if (R == 0) {
     // enough warps to cover the SMs several times: R = 4 (256-bit DP loads) for large matrices,
     // R = 2 / 1 when n_pad / R would leave the GPU short of warps (long-row matrices like DLR1)
@@ -522,6 +645,18 @@ int set_cache_policy(int stream_kind, int x_kind) {
 }
 
 int set_kernel_variant(int r, int u) {
+  // r >= 16: long-row split-j kernel with S = r - 16 threads per row (2, 4 or 8; unroll 4 or 8)
+  if (r >= 16) {
+    const int S = r - 16;
+    if (!((S == 2 || S == 4) && (u == 4 || u == 8)) && !(S == 8 && u == 4))
+      return set_error(PJDS_ERR_INVALID_ARG, "split variant: threads per row 2 or 4 with unroll 4 or 8, or 8 with 4");
+    g_split = S;
+    g_var_r = 0;
+    g_var_u = u;
+    g_pipe = false;
+    g_force_off64 = false;
+    return PJDS_OK;
+  }
   // u >= 16 encodes "software-pipelined main loop" (u - 16)
   const bool pf = u >= 16;
   if (u >= 16) u -= 16;
@@ -529,6 +664,7 @@ int set_kernel_variant(int r, int u) {
   if (r >= 8) r -= 8;
   if (!((r == 0 && u == 0) || ((r == 1 || r == 2 || r == 4) && (u == 2 || u == 4 || u == 8))))
     return set_error(PJDS_ERR_INVALID_ARG, "variant: rows_per_thread in {1,2,4}, unroll in {2,4,8} (or 0,0)");
+  g_split = 0;
   g_var_r = r;
   g_var_u = u;
   g_pipe = pf;

@@ -149,7 +149,7 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
   LZ_TRY(cudaMalloc(&u0, vb ? vb : 16));
   LZ_TRY(cudaMalloc(&u1, vb ? vb : 16));
   LZ_TRY(cudaMalloc(&y, vb ? vb : 16));
-  const int64_t np_max = std::max<int64_t>(kRedCTAs, A->h.n_pad / 256 + 1);
+  const int64_t np_max = std::max<int64_t>(kRedCTAs, A->h.n_pad / 32 + 1);  // <= 8 threads per row
   LZ_TRY(cudaMalloc(&part, np_max * sizeof(double)));
   LZ_TRY(cudaMalloc(&scal, (size_t)(3 * m + 1) * sizeof(double)));
   LZ_TRY(cudaMemsetAsync(scal, 0, (size_t)(3 * m + 1) * sizeof(double), user));

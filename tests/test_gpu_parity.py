@@ -312,6 +312,48 @@ def test_kernel_variants_bitwise(pj, variant, dtype):
         L.pjds_set_kernel_variant(0, 0)
 
 
+@pytest.mark.parametrize("variant", [(18, 4), (18, 8), (20, 4), (20, 8), (24, 4)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_split_variant_bitwise(pj, variant, dtype):
+    """Long-row split-j kernel (knob 16 + S threads per row): equal to the oracle's split-chain
+    arithmetic (S interleaved FMA chains + pairwise tree) bit for bit, and within O2; both bases,
+    ragged lengths, a row wider than the staged col_start, and the dist (y +=) store path."""
+    L = pj.lib()
+    S = variant[0] - 16
+    try:
+        assert L.pjds_set_kernel_variant(*variant) == 0
+        for kind, n, br, kw in (("random", 3001, 32, dict(max=300)), ("empty_rows", 999, 64, {}),
+                                ("clustered", 4100, 128, {}), ("adversarial", 3000, 32, {})):
+            _, rp, col, val = inputs.small(kind, n, seed=7, dtype=dtype, **kw)
+            x = inputs.vector(n, dtype)
+            want = oracle.spmv_split_chain(n, rp, col, val, x, S)
+            for sym in (False, True):
+                A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, symmetric=sym)
+                y = torch.full((n,), float("nan"), dtype=torch.float64 if dtype == np.float64 else torch.float32,
+                               device="cuda")
+                perm = A.export()["perm"]
+                A.spmv(y, tdev(x[perm] if sym else x))
+                yh = y.cpu().numpy()
+                if sym:
+                    yo = np.empty(n, dtype=yh.dtype)
+                    yo[perm] = yh
+                    yh = yo
+                check_y(yh, n, rp, col, val, x, exact=False)
+                assert np.array_equal(yh, want), (kind, sym)
+        n = 3000
+        _, rp, col, val = inputs.small("random", n, seed=9, max=200, dtype=dtype)
+        x = inputs.vector(n, dtype)
+        offs = np.array([0, 1000, 2000, 3000], np.int64)
+        hs = pj.DistPjds.create_group(n, rp, col, val, offs)
+        xs = [tdev(x[offs[r]:offs[r + 1]]) for r in range(3)]
+        ys = [torch.empty(1000, dtype=xs[0].dtype, device="cuda") for _ in range(3)]
+        pj.DistPjds.group_spmv(hs, ys, xs)
+        torch.cuda.synchronize()
+        check_y(np.concatenate([t.cpu().numpy() for t in ys]), n, rp, col, val, x, exact=False)
+    finally:
+        L.pjds_set_kernel_variant(0, 0)
+
+
 def test_permute_and_symmetric_host_e2e(pj):
     """Basis change kernels and the e2e host path of the permuted-basis mode."""
     n, rp, col, val = inputs.config_crs("C1")

@@ -119,3 +119,28 @@ def test_gpu_lanczos_breakdown_and_zero_start():
     assert a[0] == ra[0] == 2.0 and b[0] == rb[0] == 0.0
     with pytest.raises(pj.PjdsError):
         A.lanczos(torch.zeros(n, dtype=torch.float64, device="cuda"), 5)
+
+
+@pytest.mark.gpu
+def test_gpu_lanczos_split_variant():
+    """The fused alpha epilogue of the long-row split-j kernel (knob 16 + S) in the Lanczos driver."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    import paper_1112_5588_b200 as pj
+    n, rp, col, val = sym_matrix(3000, 6)
+    v0 = inputs.vector(n, seed=78)
+    ra, rb = olz.lanczos(n, rp, col, val, v0, 30)
+    L = pj.lib()
+    try:
+        for S in (2, 4, 8):
+            assert L.pjds_set_kernel_variant(16 + S, 4) == 0
+            A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+            perm = A.export()["perm"]
+            a, b, steps = A.lanczos(torch.from_numpy(v0[perm].copy()).cuda(), 30)
+            scale = max(np.abs(ra).max(), np.abs(rb).max())
+            assert steps == 30
+            assert np.abs(a[:10] - ra[:10]).max() <= 1e-10 * scale, S
+            assert np.abs(b[:10] - rb[:10]).max() <= 1e-10 * scale, S
+    finally:
+        L.pjds_set_kernel_variant(0, 0)

@@ -142,3 +142,43 @@ def test_crs_baseline_threads_identical():
     y1 = oracle.spmv_crs(g.n, rp, col, val, x, nthreads=1)
     y4 = oracle.spmv_crs(g.n, rp, col, val, x, nthreads=4)
     assert np.array_equal(y1, y4)
+
+
+def test_split_chain_order_by_hand():
+    """oracle_spmv_split_chain (the long-row kernel's arithmetic): interleaved sub-chains and the
+    pairwise tree, on exactly representable cases (x = 1) where each order gives a different value.
+      row0 = [2^53, 1, -2^53, 1]: single chain 1 (the first +1 is absorbed); S=2 interleaved:
+             p0 = 2^53-2^53 = 0, p1 = 1+1 = 2 -> 2 (a contiguous split would give 1);
+             S=4: (2^53+1 -> 2^53) + (-2^53+1) = 1.
+      row1 = [2^53, 1, 1, -2^53]: single chain 0; S=2: 2^53 + -(2^53-1) = 1; S=4 tree 1
+             (a left-to-right sum of the four partials would give 0).
+      row2 = [(col1,-1), (col0, 0), (col0, a)] with x0 = 1-2^-30, x1 = 1, a = 1+2^-30, S=2:
+             p0 = fma(a, x0, fma(-1, 1, 0)) = -2^-60 exactly (fused), p1 = 0 -> -2^-60."""
+    a = 1 + 2.0 ** -30
+    B = 2.0 ** 53
+    rp = np.array([0, 4, 8, 11])
+    col = np.array([0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0], np.int32)
+    val = np.array([B, 1, -B, 1, B, 1, 1, -B, -1, 0, a])
+    x = np.array([1.0, 1.0])
+    assert oracle.spmv_split_chain(2, rp[:3], col[:8], val[:8], x, 1).tolist() == [1.0, 0.0]
+    assert oracle.spmv_split_chain(2, rp[:3], col[:8], val[:8], x, 2).tolist() == [2.0, 1.0]
+    assert oracle.spmv_split_chain(2, rp[:3], col[:8], val[:8], x, 4).tolist() == [1.0, 1.0]
+    x2 = np.array([1 - 2.0 ** -30, 1.0])
+    y = oracle.spmv_split_chain(3, rp, col, val, x2, 2)
+    assert y[2] == -(2.0 ** -60)
+    # S = 1 is the single chain (O3)
+    _, rp3, col3, val3 = inputs.small("random", 500, seed=3, max=60)
+    xv = inputs.vector(500)
+    assert np.array_equal(oracle.spmv_split_chain(500, rp3, col3, val3, xv, 1),
+                          oracle.spmv_chain(500, rp3, col3, val3, xv))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("S", [2, 4, 8])
+def test_split_chain_within_bound(dtype, S):
+    """Any summation order obeys the O2 bound (gamma_n holds for every evaluation tree)."""
+    _, rp, col, val = inputs.small("random", 800, seed=S, max=300, dtype=dtype)
+    x = inputs.vector(800, dtype)
+    y = oracle.spmv_split_chain(800, rp, col, val, x, S)
+    yl, b = oracle.spmv_ld(800, rp, col, val, x)
+    assert oracle.acceptance(y, yl, b, np.diff(rp), dtype).all()
