@@ -149,12 +149,14 @@ def _allreduce(dist, t, op):
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
-def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1, threads: int = 0):
+def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1, threads: int = 0,
+                warmup: int = 1):
     """The oracle's plain CRS loop (oracle_spmv_crs: OpenMP static over rows, all visible cores or
     `threads`), repeated until the time budget is spent.  Returns (median s per product, reps, cores, total s)."""
     import oracle
     cores = threads or len(os.sched_getaffinity(0))
-    oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)  # warm-up
+    for _ in range(max(warmup, 1)):
+        oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)
     ts = []
     t_end = time.perf_counter() + budget_s
     while (time.perf_counter() < t_end and len(ts) < max_reps) or len(ts) < min_reps:
@@ -508,12 +510,13 @@ def reference_arm(a, world, npdt):
     rp, col, val = g.crs(dtype=npdt)
     x = inputs.vector(g.n, npdt)
     nnz = int(rp[-1])
-    t, reps, cores, tot = time_oracle(g.n, rp, col, val, x, budget_s=120.0, max_reps=a.steps)
+    w = max(a.warmup, 3)
+    t, reps, cores, tot = time_oracle(g.n, rp, col, val, x, budget_s=120.0, max_reps=a.steps, warmup=w)
     v = 2.0 * nnz / t / 1e9
     sample = f"whole {a.config} matrix ({nnz} nnz) per step, {reps} steps (median), oracle_spmv_crs"
     print(json.dumps({
         "impl": "reference", "metric": METRIC,
-        "value": round(v, 3), "unit": "GFlop/s", "n_gpus": world, "steps": reps, "warmup": 1,
+        "value": round(v, 3), "unit": "GFlop/s", "n_gpus": world, "steps": reps, "warmup": w,
         "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": a.dtype, "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
         "config": {"workload": f"{a.config}: {CONFIG_DESC[a.config]}, nnz={nnz}, CPU oracle CRS"},
