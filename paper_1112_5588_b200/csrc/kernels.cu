@@ -131,6 +131,18 @@ template <> struct Vec<int, 4> {
   }
 };
 
+// IL (lane-interleaved rows): the R rows of a thread are 32 apart (row warp_k0 + lane + 32 r), so
+// one gather instruction covers 32 consecutive rows; val/col then take R scalar loads per slot.
+template <bool IL, typename T, int R>
+__device__ __forceinline__ void load_rows(Vec<T, R>& v, const T* p, uint64_t pol) {
+  if constexpr (IL) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v.v[r] = ld_stream(p + 32 * r, pol);
+  } else {
+    v.load(p, pol);
+  }
+}
+
 constexpr int kThreads = 256;
 constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
 // Register budget: plain __launch_bounds__(256) (48 registers for the R=4 DP kernel).  Measured:
@@ -151,7 +163,7 @@ enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 
 // PIPE: software-pipelined main loop (next chunk's val/col loads in flight during the current
 // chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
-template <typename T, typename Off, int R, int U, int MODE, bool PIPE>
+template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
@@ -161,7 +173,8 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   // execution order of the CTA tiles (storage order, or by original row; results are identical)
   const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
   const int64_t t = tile * kThreads + threadIdx.x;
-  const int64_t k0 = t * R;
+  constexpr int RS = IL ? 32 : 1;  // distance between a thread's rows
+  const int64_t k0 = IL ? ((t & ~int64_t(31)) * R + (t & 31)) : t * R;
   const int64_t cta_k0 = tile * kThreads * R;
   const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
   // sort window of this CTA (CTAs never straddle windows: sigma is a multiple of the tile size);
@@ -191,8 +204,8 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const Off o = cs(u) + (Off)k0;
-      va[u].load(val + o, pol_s);
-      ca[u].load(col + o, pol_s);
+      load_rows<IL>(va[u], val + o, pol_s);
+      load_rows<IL>(ca[u], col + o, pol_s);
     }
     for (;;) {
       T xv[U][R];
@@ -208,8 +221,8 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const Off o = cs(jn + u) + (Off)k0;
-          vb[u].load(val + o, pol_s);
-          cb[u].load(col + o, pol_s);
+          load_rows<IL>(vb[u], val + o, pol_s);
+          load_rows<IL>(cb[u], col + o, pol_s);
         }
       }
 #pragma unroll
@@ -231,8 +244,8 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const Off o = cs(j + u) + (Off)k0;
-      v[u].load(val + o, pol_s);
-      c[u].load(col + o, pol_s);
+      load_rows<IL>(v[u], val + o, pol_s);
+      load_rows<IL>(c[u], col + o, pol_s);
     }
     T xv[U][R];
 #pragma unroll
@@ -251,8 +264,8 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
     for (int u = 0; u < U; ++u)
       if (j + u < len) {
         const Off o = cs(j + u) + (Off)k0;
-        v[u].load(val + o, pol_s);
-        c[u].load(col + o, pol_s);
+        load_rows<IL>(v[u], val + o, pol_s);
+        load_rows<IL>(c[u], col + o, pol_s);
       }
     T xv[U][R];
 #pragma unroll
@@ -268,7 +281,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t k = k0 + r;
+    const int64_t k = k0 + r * RS;
     if (k < n) {
       if (MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) {
         y[k] = acc[r];
@@ -286,7 +299,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
     if (active)
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (k0 + r < n) d = fma((double)acc[r], (double)x[k0 + r], d);
+        if (k0 + r * RS < n) d = fma((double)acc[r], (double)x[k0 + r * RS], d);
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
     __syncthreads();
@@ -307,7 +320,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 // Not the single-chain order of reading 14: checked bitwise against oracle_spmv_split_chain and
 // against the O2 bound.
 template <typename T, typename Off, int S, int U, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 pjds_spmv_split_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                        const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                        T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, double* __restrict__ dot_part,
@@ -357,15 +370,12 @@ pjds_spmv_split_kernel(const T* __restrict__ val, const int* __restrict__ col, c
   __syncthreads();
   const bool owner = active && sub == 0 && k < n;
   if (sub == 0) {
-    // pairwise tree over the group's S partials (warps w .. w+S-1)
-    T p[S];
-#pragma unroll
-    for (int q = 0; q < S; ++q) p[q] = s_part[w + q][lane];
-#pragma unroll
-    for (int step = 1; step < S; step *= 2)
-#pragma unroll
-      for (int q = 0; q + step < S; q += 2 * step) p[q] = p[q] + p[q + step];
-    acc = p[0];
+    // pairwise tree over the group's S partials (warps w .. w+S-1), written out so that no
+    // partial needs a local-memory array
+    auto P = [&](int q) -> T { return s_part[w + q][lane]; };
+    if constexpr (S == 2) acc = P(0) + P(1);
+    else if constexpr (S == 4) acc = (P(0) + P(1)) + (P(2) + P(3));
+    else acc = ((P(0) + P(1)) + (P(2) + P(3))) + ((P(4) + P(5)) + (P(6) + P(7)));
     if (owner) {
       if (MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) {
         y[k] = acc;
@@ -408,6 +418,7 @@ int set_tile_order_impl(int mode) {
   return PJDS_OK;
 }
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
+static bool g_il = false;    // lane-interleaved rows (variant knob unroll + 32; needs b_r % (32 R) == 0)
 
 template <typename T, typename Off, int R, int U>
 int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part, int64_t* nparts,
@@ -425,13 +436,15 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
                       (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
                        (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(A, R, &order));
-#define PJDS_LAUNCH_PF(M, PF)                                                                            \
-  pjds_spmv_kernel<T, Off, R, U, M, PF><<<(unsigned)grid, kThreads, 0, s>>>(                            \
+#define PJDS_LAUNCH_PF(M, PF, IL)                                                                        \
+  pjds_spmv_kernel<T, Off, R, U, M, PF, IL><<<(unsigned)grid, kThreads, 0, s>>>(                        \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part, h.sigma, \
       A->d_wcs_off)
-#define PJDS_LAUNCH(M)             \
-  if (pipe) PJDS_LAUNCH_PF(M, true); \
-  else PJDS_LAUNCH_PF(M, false)
+  const bool il = g_il && R > 1 && h.br % (32 * R) == 0;
+#define PJDS_LAUNCH(M)                    \
+  if (pipe) PJDS_LAUNCH_PF(M, true, false); \
+  else if (il) PJDS_LAUNCH_PF(M, false, true); \
+  else PJDS_LAUNCH_PF(M, false, false)
   if (mode == STORE_DIRECT) {
     PJDS_LAUNCH(STORE_DIRECT);
   } else if (mode == STORE_DIRECT_DOT) {
@@ -654,10 +667,13 @@ int set_kernel_variant(int r, int u) {
     g_var_r = 0;
     g_var_u = u;
     g_pipe = false;
+    g_il = false;
     g_force_off64 = false;
     return PJDS_OK;
   }
-  // u >= 16 encodes "software-pipelined main loop" (u - 16)
+  // u >= 32: lane-interleaved rows (u - 32); u >= 16 encodes "software-pipelined main loop" (u - 16)
+  const bool il = u >= 32;
+  if (u >= 32) u -= 32;
   const bool pf = u >= 16;
   if (u >= 16) u -= 16;
   const bool off64 = r >= 8;  // rows_per_thread + 8: force 64-bit jagged offsets
@@ -668,6 +684,7 @@ int set_kernel_variant(int r, int u) {
   g_var_r = r;
   g_var_u = u;
   g_pipe = pf;
+  g_il = il;
   g_force_off64 = off64;
   return PJDS_OK;
 }

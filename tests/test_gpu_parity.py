@@ -280,11 +280,12 @@ def test_misuse_errors(pj):
         A.spmv(torch.empty(n, dtype=torch.float32, device="cuda"), x)
 
 
-@pytest.mark.parametrize("variant", [(1, 8), (2, 4), (2, 8), (4, 2), (4, 4), (9, 8), (10, 4), (12, 2), (4, 18)])
+@pytest.mark.parametrize("variant", [(1, 8), (2, 4), (2, 8), (4, 2), (4, 4), (9, 8), (10, 4), (12, 2), (4, 18),
+                                     (4, 34), (2, 36), (4, 36), (12, 34)])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_kernel_variants_bitwise(pj, variant, dtype):
     """Every (rows per thread, unroll) variant gives the same per-row FMA chain (R+8: 64-bit offsets,
-    U+16: with the L2 bulk prefetch)."""
+    U+16: software-pipelined, U+32: lane-interleaved rows, active where b_r % 32R == 0)."""
     L = pj.lib()
     try:
         assert L.pjds_set_kernel_variant(*variant) == 0
