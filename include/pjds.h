@@ -362,6 +362,15 @@ int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gb
    bound. */
 int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
 
+/* Execution order of the CTA tiles of one handle (used whenever the tile order is on: mode 1, or
+   mode 2's automatic choice — pjds_set_tile_order): tiles run sorted (stably) by key[orig] of their
+   first row's ORIGINAL index, e.g. a 2-D (phonon window, electronic block) key for HMEp-type
+   Kronecker matrices so that RHS entries shared across blocks are reused while in L2 (PAPER.md
+   L246-249).  key: host int64[n] (copied) or NULL to restore the default key (the original index
+   itself).  Only the order of independent tiles changes: results are bit-identical.  Not safe
+   while a product on this handle is running. */
+int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n);
+
 /* Tuning knob (process-wide): L2 eviction priority of the pJDS kernel's streamed val/col loads
    and of its x gathers; kinds 0 evict_normal, 1 evict_first, 2 evict_last, 3 evict_unchanged.
    Default (1, 2).  Results are unaffected. */

@@ -145,6 +145,16 @@ class PjdsMatrix:
              beta.ctypes.data, ctypes.byref(steps), _stream_ptr(stream))
         return alpha, beta, steps.value
 
+    def set_tile_keys(self, keys=None):
+        """Tile execution order by a key per ORIGINAL row (pjds_set_tile_keys); None restores the
+        default (original index).  Results are unchanged; only L2 reuse can differ."""
+        if keys is None:
+            call("pjds_set_tile_keys", self._h, None, 0)
+        else:
+            k = np.ascontiguousarray(keys, dtype=np.int64)
+            call("pjds_set_tile_keys", self._h, k.ctypes.data, len(k))
+        return self
+
     def footprint(self) -> dict:
         """Bytes per component (pjds_footprint: values, indices, col_start, block_len, perm)."""
         f = _lib.Footprint()

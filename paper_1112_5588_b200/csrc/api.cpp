@@ -417,6 +417,18 @@ int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll) {
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind) { return set_cache_policy(stream_kind, x_kind); }
 int pjds_set_tile_order(int32_t mode) { return set_tile_order(mode); }
 
+int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n) {
+  if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: NULL handle");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: handle is host-only");
+  if (key && n != A->h.n) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: need one key per row");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (A->device >= 0) cudaSetDevice(A->device);
+  const int s = build_tile_orders(A, key);
+  if (prev >= 0) cudaSetDevice(prev);
+  return s;
+}
+
 int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs) {
   if (!copy_gbs || !read_gbs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_bw_probe: NULL argument");
   return bw_probe(bytes, reps, copy_gbs, read_gbs);

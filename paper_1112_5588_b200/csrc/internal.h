@@ -97,7 +97,7 @@ struct ellr_mat {
 namespace pjds {
 int upload_pjds(pjds_mat* A, const int32_t* store_map /* optional: perm composed with this */);
 int free_pjds_device(pjds_mat* A);
-int build_tile_orders(pjds_mat* A);
+int build_tile_orders(pjds_mat* A, const int64_t* row_key = nullptr);
 
 // ---- kernel launchers (kernels.cu) -----------------------------------------------------------
 int launch_pjds_spmv(const pjds_mat* A, void* y, const void* x, cudaStream_t s, bool accumulate);

@@ -616,7 +616,10 @@ __global__ void read_kernel(const int4* __restrict__ a, int64_t n, int* __restri
 
 // Tiles (CTAs of 256 R consecutive sorted rows) ordered by the original index of their first row,
 // one table per rows-per-thread variant R in {1, 2, 4}; built once at upload.
-int build_tile_orders(pjds_mat* A) {
+// Tile execution orders for R = 1, 2, 4: tiles sorted (stably) by the key of their first row's
+// original index — the index itself by default, or a caller key per original row
+// (pjds_set_tile_keys).  Only the order of independent CTAs changes, never a result.
+int build_tile_orders(pjds_mat* A, const int64_t* row_key) {
   const auto& h = A->h;
   const int Rs[3] = {1, 2, 4};
   for (int slot = 0; slot < 3; ++slot) {
@@ -625,12 +628,12 @@ int build_tile_orders(pjds_mat* A) {
     std::vector<int64_t> key(tiles);
     for (int64_t t = 0; t < tiles; ++t) {
       const int64_t k = t * rows;
-      key[t] = k < h.n ? (int64_t)h.perm[k] : INT64_MAX;
+      key[t] = k < h.n ? (row_key ? row_key[h.perm[k]] : (int64_t)h.perm[k]) : INT64_MAX;
     }
     std::vector<int32_t> ord(tiles);
     for (int64_t t = 0; t < tiles; ++t) ord[t] = (int32_t)t;
     std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_order[slot], tiles * 4));
+    if (!A->d_order[slot]) PJDS_CUDA_TRY(cudaMalloc(&A->d_order[slot], tiles * 4));
     PJDS_CUDA_TRY(cudaMemcpy(A->d_order[slot], ord.data(), tiles * 4, cudaMemcpyHostToDevice));
   }
   return PJDS_OK;

@@ -391,6 +391,29 @@ def test_tile_order_bitwise(pj, order):
         L.pjds_set_tile_order(2)
 
 
+def test_tile_keys_bitwise(pj):
+    """pjds_set_tile_keys (user execution order: a random key, the HMEp 2-D window key, and back to
+    the default) never changes a row's chain; a wrong-length key is rejected."""
+    L = pj.lib()
+    n, rp, col, val = inputs.config_crs("C1")
+    x = inputs.vector(n)
+    rng = np.random.default_rng(3)
+    r = np.arange(n, dtype=np.int64)
+    try:
+        assert L.pjds_set_tile_order(1) == 0
+        for sym in (False, True):
+            A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=sym)
+            for keys in (rng.permutation(n).astype(np.int64), ((r % 1024) // 256) * n + r, None):
+                A.set_tile_keys(keys)
+                y = np.empty(n)
+                A.spmv_host(y, x)
+                check_y(y, n, rp, col, val, x)
+            with pytest.raises(pj.PjdsError):
+                A.set_tile_keys(np.zeros(n - 1, np.int64))
+    finally:
+        L.pjds_set_tile_order(2)
+
+
 @pytest.mark.parametrize("symmetric", [False, True])
 def test_spmv_host_batch_pipelined(pj, symmetric):
     """Pipelined host-buffer products (double-buffered staging, copy streams) equal the oracle."""

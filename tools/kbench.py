@@ -30,6 +30,8 @@ p.add_argument("--variants", default="0x0")
 p.add_argument("--policies", default="1x2")
 p.add_argument("--orders", default="2")
 p.add_argument("--sigmas", default="0")
+p.add_argument("--keys", default="none", help="tile keys: none (original index) or wW = HMEp phonon window of W rows")
+SEG = {"C1": 1024, "C3": 15504, "C5": 142506}
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
@@ -51,7 +53,15 @@ for cfg in a.configs.split(","):
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
           pj.bw_probe(1 << 30, 20)  # host-side conversion leaves the GPU idle: re-raise clocks
-          for var, polk, order in [(v, q, o) for v in a.variants.split(",") for q in a.policies.split(",") for o in a.orders.split(",")]:
+          for var, polk, order, kspec in [(v, q, o, kk) for v in a.variants.split(",") for q in a.policies.split(",")
+                                          for o in a.orders.split(",") for kk in a.keys.split(",")]:
+            if fmt.startswith("pjds"):
+                if kspec == "none":
+                    A.set_tile_keys(None)
+                else:  # 2-D order: phonon window of the row, then the original index
+                    W, P = int(kspec[1:]), SEG[cfg]
+                    r = np.arange(n, dtype=np.int64)
+                    A.set_tile_keys(((r % P) // W) * n + r)
             pj.lib().pjds_set_tile_order(int(order))
             vr, vu = map(int, var.split("x"))
             pj.lib().pjds_set_kernel_variant(vr, vu)
@@ -68,7 +78,7 @@ for cfg in a.configs.split(","):
             ck = clocks()
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
-            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "keys": kspec, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
                               "stored_bytes": A.info.get("bytes_total"), "clk": ck}), flush=True)
           del A
