@@ -178,7 +178,7 @@ int hmep_row(const Gen& g, int64_t r, int32_t* cols) {
 }
 
 // ---------------------------------------------------------------- HMEp banded (C1)
-int hmep_banded_row(const Gen& g, int64_t r, int32_t* cols) {
+int hmep_banded_row(const Gen&, int64_t r, int32_t* cols) {
   const int PB = 1024, NB = 16;
   int b = (int)(r / PB), p = (int)(r % PB);
   static const int offs[6] = {1, 2, 5, 7, 11, 13};
