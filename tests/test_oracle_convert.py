@@ -3,7 +3,6 @@ utilisation counters): the hand-derived G1 example, the paper
 (PAPER.md L256-266), SPEC acceptance 1/2, and invariants checked by independent
 recounts."""
 from collections import Counter
-from fractions import Fraction
 
 import numpy as np
 import pytest
