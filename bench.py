@@ -64,6 +64,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-compare", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=30)
+    p.add_argument("--tile-window", type=int, default=0,
+                   help="HMEp configs, N=1: run tiles by (phonon window of this many rows, original row); 0 = off")
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
     p.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
@@ -229,6 +231,10 @@ def main():
             A = pj.EllrMatrix.from_crs(n, rp, col, val)
         else:
             A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=a.block_rows, symmetric=permuted)
+            if a.tile_window:  # opt-in 2-D (phonon window, original row) tile order for HMEp
+                r_ = np.arange(n, dtype=np.int64)
+                A.set_tile_keys(((r_ % SEGMENT[a.config]) // a.tile_window) * n + r_)
+                del r_
             st = A.info
             ell_rows = (n + 31) // 32 * 32
             ell_entries = ell_rows * st["len_max"]
@@ -471,6 +477,7 @@ def main():
                        "parallelism": f"row-partition r{world}" if world > 1 else "single GPU",
                        "overlap": (not a.no_overlap) if use_dist else None,
                        "transport": a.transport if use_dist else None,
+                       "tile_window": a.tile_window or None,
                        "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
             "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
