@@ -351,7 +351,8 @@ def main():
     achieved = b_min / t_s / 1e9 / world  # per GPU
     peak = peak_file if peak_file else max(probe_copy, probe_read)
 
-    traffic_key = f"{a.config}/{a.dtype}/{a.basis}" + ("" if a.block_rows == 32 else f"/br{a.block_rows}")
+    traffic_key = (f"{a.config}/{a.dtype}/{a.basis}" + ("" if a.block_rows == 32 else f"/br{a.block_rows}")
+                   + (f"/tw{a.tile_window}" if a.tile_window else ""))
 
     # side-by-side kernels on the same matrix (N=1): rows-only pJDS and ELLPACK-R
     if not use_dist and a.impl == "pjds" and not a.no_compare:
