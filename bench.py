@@ -30,6 +30,7 @@ import os
 import sys
 import threading
 import time
+import warnings
 
 import numpy as np
 
@@ -374,6 +375,19 @@ def main():
                              "bytes": B.info["bytes_total"]}
             del B
             torch.cuda.synchronize()
+        # NVIDIA's library CRS SpMV on the same matrix and the same device (cuSPARSE via torch.sparse
+        # CSR): the vendor baseline beside the pJDS kernel, not part of the product path
+        warnings.filterwarnings("ignore", message="Sparse CSR tensor support is in beta")
+        C = torch.sparse_csr_tensor(torch.from_numpy(rp.astype(np.int32)).to(dev), torch.from_numpy(col).to(dev),
+                                    torch.from_numpy(val).to(dev), size=(n, n), check_invariants=False)
+        for _ in range(3):
+            torch.mv(C, x0)
+        mb = timed(lambda: torch.mv(C, x0), 20)
+        compare["cusparse_csr"] = {"GFlop/s": round(2.0 * nnz / (mb * 1e-3) / 1e9, 1), "ms": round(mb, 4),
+                                   "frac": round(b_min / (mb * 1e-3) / 1e9 / peak, 4),
+                                   "bytes": int(nnz * (sv + 4) + (n + 1) * 4)}
+        del C
+        torch.cuda.synchronize()
         del x0
     del col, val
 
