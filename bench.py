@@ -69,8 +69,9 @@ def parse():
                    help="HMEp configs, N=1: run tiles by (phonon window of this many rows, original row); 0 = off")
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
-    p.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
-                   help="dist halo exchange: NCCL send/recv on a side stream, or the fused gather+put P2P kernel")
+    p.add_argument("--transport", default="nccl", choices=["nccl", "p2p", "direct"],
+                   help="dist: NCCL send/recv on a side stream, the fused gather+put P2P kernel, or DIRECT "
+                        "(no exchange: one kernel whose nonlocal gathers read the owners' x windows)")
     return p.parse_args()
 
 
@@ -264,6 +265,10 @@ def main():
         xp = torch.empty_like(x)
         (D if use_dist else A).to_permuted(xp, x)  # once, before the "iterative scheme"
         x = xp
+    if use_dist and a.transport == "direct":  # x lives in the exported window: no per-call copy
+        w = D.x_window()
+        w.copy_(x)
+        x = w
     t_setup = time.perf_counter() - t_setup
 
     # roofline denominator measured in this run (copy and read streams)

@@ -247,11 +247,27 @@ enum {
   PJDS_TRANSPORT_NCCL = 0,  /* one process per GPU; nccl_unique_id = 128-byte ncclUniqueId */
   PJDS_TRANSPORT_LOCAL = 1, /* all ranks' handles in this process (pjds_dist_group_spmv);
                                halo moved with device-to-device copies; test harness */
-  PJDS_TRANSPORT_P2P = 2    /* one process per GPU (or several per GPU), no NCCL per call: a fused
+  PJDS_TRANSPORT_P2P = 2,   /* one process per GPU (or several per GPU), no NCCL per call: a fused
                                gather+put kernel stores the send entries straight into the
                                receivers' halo buffers through CUDA-IPC mappings (NVLink P2P),
                                release/acquire flags order put -> nonlocal part -> buffer reuse.
                                Connect with pjds_dist_p2p_export / _connect after create. */
+  PJDS_TRANSPORT_DIRECT = 3 /* one process per GPU (or several per GPU): NO exchange step.  ONE pJDS
+                               matrix over the full local rows (CRS order kept within each row, so
+                               y is bitwise the unsplit FMA chain); its nonlocal columns address the
+                               owners' x windows directly (CUDA-IPC mapped peer memory: NVLink loads
+                               between GPUs), so the transfer happens inside the spMVM kernel, tile
+                               by tile, overlapped with the local val/col stream -- the B200 form of
+                               the paper's communication/computation overlap.
+                               Per call: x -> window (skipped if x IS the window), release "ready"
+                               to the readers, acquire the owners' "ready", kernel, release "done"
+                               to the owners, acquire the readers' "done" (when the call completes
+                               on the stream nobody reads this rank's window any more).  Setup:
+                               create -> pjds_dist_direct_positions -> caller all_to_all ->
+                               pjds_dist_p2p_export / all_gather -> pjds_dist_direct_connect.
+                               Needs nranks <= 64 and nranks * 2^ceil(log2(max rows per rank)) <=
+                               2^31 (column code (owner << shift) | position in 32 bits);
+                               PJDS_NO_OVERLAP has no meaning here (there is nothing to overlap). */
 };
 enum {
   PJDS_NO_OVERLAP = 1u, /* serialise exchange and compute (vector mode) */
@@ -284,6 +300,21 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t plan, const void* val_loc, in
 int pjds_dist_p2p_export(pjds_dist_t D, void* blob, int64_t* bytes);
 int pjds_dist_p2p_connect(pjds_dist_t D, const void* blobs, int64_t blob_bytes);
 int pjds_dist_p2p_check(pjds_dist_t D, int32_t* timed_out);
+/* PJDS_TRANSPORT_DIRECT setup and use.
+   pjds_dist_direct_positions: pos[send_total] = the position in this rank's x window of every
+     entry of send_cols (same order): local row id, or its index in the local permuted basis
+     (PJDS_PERM_SYMMETRIC).  The caller returns each peer's slice to that peer (all_to_all).
+   pjds_dist_direct_connect (collective in effect): halo_pos[halo] = for every halo slot (owner-
+     ordered, as pjds_dist_plan_recv), its position in the owner's window, i.e. the owner's
+     pjds_dist_direct_positions entries for this rank; blobs = nranks pjds_dist_p2p_export blobs in
+     rank order.  Opens the peers' windows, rewrites the matrix's column codes and uploads it.
+     INVALID_ARG if a position lies outside the owner's rows.
+   pjds_dist_x_window: *x_window = this rank's exported x window (device, n_loc entries of the
+     handle dtype, in the basis of the handle).  Compute x there to skip the per-call copy; rewrite
+     it only between calls (stream order). */
+int pjds_dist_direct_positions(pjds_dist_t D, int32_t* pos);
+int pjds_dist_direct_connect(pjds_dist_t D, const int32_t* halo_pos, const void* blobs, int64_t blob_bytes);
+int pjds_dist_x_window(pjds_dist_t D, void** x_window);
 /* Basis change of a local vector for PJDS_PERM_SYMMETRIC dist handles (see pjds_permute). */
 int pjds_dist_permute(pjds_dist_t D, void* dst, const void* src, int32_t direction, void* stream);
 /* y_loc = A[rows of this rank, :] x ; x_loc / y_loc device pointers of length n_loc. */

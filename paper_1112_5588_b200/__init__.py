@@ -299,6 +299,27 @@ def exchange_lists(recv_counts, recv_cols, group=None):
     return send_counts, out.cpu().numpy().astype(np.int32)
 
 
+def _alltoallv_i32(arr, in_splits, out_splits, group=None):
+    """all_to_all_single of an int32 array with the given splits (setup-time plumbing)."""
+    import torch
+    import torch.distributed as dist
+    dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
+           else torch.device("cpu"))
+    inp = torch.as_tensor(np.ascontiguousarray(arr, np.int32), device=dev)
+    out = torch.empty(int(np.sum(out_splits)), dtype=torch.int32, device=dev)
+    dist.all_to_all_single(out, inp, output_split_sizes=[int(v) for v in out_splits],
+                           input_split_sizes=[int(v) for v in in_splits], group=group)
+    return out.cpu().numpy().astype(np.int32)
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of library-owned device memory (no ownership)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
 class DistPjds:
     """Row-partitioned distributed pJDS spMVM (§3): local part overlapped with the
     NCCL halo exchange on a high-priority side stream, then the nonlocal part (y +=)."""
@@ -317,8 +338,10 @@ class DistPjds:
                permuted: bool = False, transport: str = "nccl"):
         """Collective over the torch.distributed default (or given) group: one rank per GPU.
         permuted: x_loc / y_loc live in the local permuted basis (to_permuted / from_permuted).
-        transport: "nccl" (grouped send/recv on a side stream) or "p2p" (fused gather+put kernel
-        into the peers' halo buffers through CUDA-IPC mappings, no NCCL per call)."""
+        transport: "nccl" (grouped send/recv on a side stream), "p2p" (fused gather+put kernel
+        into the peers' halo buffers through CUDA-IPC mappings, no NCCL per call) or "direct" (no
+        exchange step: ONE kernel per call whose nonlocal gathers read the owners' x windows
+        through CUDA-IPC mappings; place x in `x_window()` to skip the per-call copy)."""
         import torch.distributed as dist
         R, rank = dist.get_world_size(group), dist.get_rank(group)
         val_loc = np.ascontiguousarray(val_loc)
@@ -326,7 +349,7 @@ class DistPjds:
         rc, rcols = plan.recv()
         sc, scols = exchange_lists(rc, rcols, group)
         uid = (ctypes.c_char * 128)()
-        tr = {"nccl": PJDS_TRANSPORT_NCCL, "p2p": _lib.PJDS_TRANSPORT_P2P}[transport]
+        tr = {"nccl": PJDS_TRANSPORT_NCCL, "p2p": _lib.PJDS_TRANSPORT_P2P, "direct": _lib.PJDS_TRANSPORT_DIRECT}[transport]
         if R > 1 and transport == "nccl":
             call("pjds_nccl_load", _nccl_path())
             if rank == 0:
@@ -349,7 +372,31 @@ class DistPjds:
             allb = b"".join(blobs)
             call("pjds_dist_p2p_connect", h, ctypes.c_char_p(allb), nb.value)
             dist.barrier(group=group)
+        if transport == "direct":
+            # my window positions of what each peer reads from me -> that peer's halo positions
+            pos = np.zeros(max(int(sc.sum()), 1), np.int32)
+            call("pjds_dist_direct_positions", h, pos.ctypes.data)
+            halo_pos = _alltoallv_i32(pos[:int(sc.sum())], sc, rc, group)
+            nb = ctypes.c_int64()
+            call("pjds_dist_p2p_export", h, None, ctypes.byref(nb))
+            blob = (ctypes.c_char * nb.value)()
+            call("pjds_dist_p2p_export", h, blob, ctypes.byref(nb))
+            blobs = [None] * R
+            dist.all_gather_object(blobs, bytes(blob), group=group)
+            hp = np.ascontiguousarray(halo_pos if len(halo_pos) else np.zeros(1, np.int32))
+            call("pjds_dist_direct_connect", h, hp.ctypes.data, ctypes.c_char_p(b"".join(blobs)), nb.value)
+            dist.barrier(group=group)
         return obj
+
+    def x_window(self):
+        """DIRECT transport: this rank's exported x window as a torch tensor view (n_loc entries;
+        valid while the handle lives).  Compute x there (e.g. to_permuted(D.x_window(), x)) and
+        pass it to spmv to skip the per-call copy; rewrite it only between calls."""
+        import torch
+        p = ctypes.c_void_p()
+        call("pjds_dist_x_window", self._h, ctypes.byref(p))
+        ts = "<f8" if self.dtype == PJDS_F64 else "<f4"
+        return torch.as_tensor(_DeviceArray(p.value or 0, self.n_loc, ts), device="cuda")
 
     def p2p_timed_out(self) -> bool:
         v = ctypes.c_int32()

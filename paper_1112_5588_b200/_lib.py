@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libpjds.so")
 
 PJDS_F32, PJDS_F64 = 0, 1
 PJDS_PERM_ROWS, PJDS_PERM_SYMMETRIC, PJDS_HOST_ONLY = 0, 1, 2
-PJDS_TRANSPORT_NCCL, PJDS_TRANSPORT_LOCAL, PJDS_TRANSPORT_P2P = 0, 1, 2
+PJDS_TRANSPORT_NCCL, PJDS_TRANSPORT_LOCAL, PJDS_TRANSPORT_P2P, PJDS_TRANSPORT_DIRECT = 0, 1, 2, 3
 PJDS_NO_OVERLAP, PJDS_TRACE = 1, 2
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "BAD_CSR", -3: "OOM", -4: "CUDA", -5: "NCCL", -6: "UNSUPPORTED"}
 
@@ -98,6 +98,9 @@ _SIGS = {
     "pjds_dist_p2p_export": [c_p, c_p, c_p],
     "pjds_dist_p2p_connect": [c_p, c_p, c_i64],
     "pjds_dist_p2p_check": [c_p, c_p],
+    "pjds_dist_direct_positions": [c_p, c_p],
+    "pjds_dist_direct_connect": [c_p, c_p, c_p, c_i64],
+    "pjds_dist_x_window": [c_p, c_p],
     "pjds_dist_parts": [c_p, c_p, c_p],
     "pjds_dist_destroy": [c_p],
     "pjds_nccl_load": [ctypes.c_char_p],

@@ -15,6 +15,11 @@
 //               compute stream             : A_loc kernel (y = ...)      -- overlapped
 //               compute stream             : wait(comm) -> A_nl kernel (y += ..., written twice, L445)
 //             PJDS_NO_OVERLAP serialises everything on the compute stream (vector mode, L437-440).
+//   DIRECT  : (PJDS_TRANSPORT_DIRECT) no exchange step at all: ONE pJDS matrix over the full local
+//             rows whose nonlocal columns address the owners' x windows (CUDA-IPC mapped peer
+//             memory; NVLink loads between GPUs).  One kernel runs every row's whole chain, the
+//             remote gathers overlapping the local val/col stream tile by tile; flags order
+//             "owner's x ready" -> kernel -> "reader done" (end barrier: x may be rewritten after).
 #include <algorithm>
 #include <cstring>
 #include <dlfcn.h>
@@ -158,7 +163,13 @@ struct pjds_dist {
   std::vector<void*> peer_regions;              // opened IPC mappings
   bool p2p_connected = false;
   uint64_t seq = 0;
-  uint64_t* ready_flags() const { return (uint64_t*)(p2p_region + 2 * p2p_halo_bytes); }
+  size_t p2p_flags_off = 0;                     // byte offset of ready[R] in the exported region
+  // ---- DIRECT transport: region = [x window | ready[R] | done[R] | err]
+  int32_t win_shift = 0;
+  void** d_win = nullptr;                       // [kWinTable] x-window base per owner rank
+  std::vector<int32_t> dir_send_pos;            // my window position of every send entry (send order)
+  std::vector<int64_t> offsets;                 // row offsets [R+1]
+  uint64_t* ready_flags() const { return (uint64_t*)(p2p_region + p2p_flags_off); }
   uint64_t* done_flags() const { return ready_flags() + R; }
   unsigned* err_flag() const { return (unsigned*)(done_flags() + R); }
 };
@@ -188,6 +199,7 @@ int p2p_setup(pjds_dist* D, const std::vector<int32_t>& ids, const std::vector<i
   const size_t vs = vsz(D);
   D->p2p_halo_bytes = (std::max<size_t>(D->halo * vs, 16) + 255) / 256 * 256;
   D->p2p_region_bytes = 2 * D->p2p_halo_bytes + 2 * (size_t)D->R * 8 + 256;
+  D->p2p_flags_off = 2 * D->p2p_halo_bytes;
   PJDS_CUDA_TRY(cudaMalloc(&D->p2p_region, D->p2p_region_bytes));
   PJDS_CUDA_TRY(cudaMemset(D->p2p_region, 0, D->p2p_region_bytes));
   const size_t ns = D->send_peers.size(), nr = D->recv_peers.size();
@@ -206,11 +218,35 @@ int p2p_setup(pjds_dist* D, const std::vector<int32_t>& ids, const std::vector<i
   return PJDS_OK;
 }
 
+constexpr int kWinTable = 64;  // = kMaxWin of the window kernel (kernels.cu)
+
+// DIRECT transport: the IPC-exported x window + flags, the window-base table, the flag tables.
+int direct_setup(pjds_dist* D) {
+  const size_t vs = vsz(D);
+  const size_t win = (std::max<size_t>(D->n_loc * vs, 16) + 255) / 256 * 256;
+  D->p2p_flags_off = win;
+  D->p2p_region_bytes = win + 2 * (size_t)D->R * 8 + 256;
+  PJDS_CUDA_TRY(cudaMalloc(&D->p2p_region, D->p2p_region_bytes));
+  PJDS_CUDA_TRY(cudaMemset(D->p2p_region, 0, D->p2p_region_bytes));
+  const size_t ns = D->send_peers.size(), nr = D->recv_peers.size();
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_send_peers, std::max<size_t>(ns, 1) * 4));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_recv_peers, std::max<size_t>(nr, 1) * 4));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_ready_targets, std::max<size_t>(ns, 1) * sizeof(void*)));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_done_targets, std::max<size_t>(nr, 1) * sizeof(void*)));
+  PJDS_CUDA_TRY(cudaMalloc(&D->d_win, kWinTable * sizeof(void*)));
+  PJDS_CUDA_TRY(cudaMemset(D->d_win, 0, kWinTable * sizeof(void*)));
+  if (ns) PJDS_CUDA_TRY(cudaMemcpy(D->d_send_peers, D->send_peers.data(), ns * 4, cudaMemcpyHostToDevice));
+  if (nr) PJDS_CUDA_TRY(cudaMemcpy(D->d_recv_peers, D->recv_peers.data(), nr * 4, cudaMemcpyHostToDevice));
+  D->peer_regions.assign(D->R, nullptr);
+  return PJDS_OK;
+}
+
 // Fixed-size blob each rank publishes: IPC handle of its region plus its halo layout.
 constexpr int kP2PMaxRanks = 64;
 struct P2PBlob {
   cudaIpcMemHandle_t handle;
   uint64_t halo_bytes;
+  uint64_t flags_off;
   int32_t R, rank;
   int64_t recv_off[kP2PMaxRanks];
 };
@@ -346,7 +382,8 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
   if (flags & ~(uint32_t)PJDS_PERM_SYMMETRIC) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: unknown flags");
   const bool sym = flags & PJDS_PERM_SYMMETRIC;
   if (dtype != PJDS_F32 && dtype != PJDS_F64) return set_error(PJDS_ERR_INVALID_ARG, "bad dtype");
-  if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL && transport != PJDS_TRANSPORT_P2P)
+  if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL && transport != PJDS_TRANSPORT_P2P &&
+      transport != PJDS_TRANSPORT_DIRECT)
     return set_error(PJDS_ERR_INVALID_ARG, "bad transport");
   if (P->nnz_loc > 0 && !val) return set_error(PJDS_ERR_INVALID_ARG, "val is NULL");
   if (P->R > 1 && !send_counts) return set_error(PJDS_ERR_INVALID_ARG, "send_counts is NULL");
@@ -370,6 +407,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
   D->nnz_loc_part = (int64_t)P->loc_col.size(); D->nnz_nl_part = (int64_t)P->nl_col.size();
   D->rows_nl = (int64_t)P->rows_nl.size();
   D->recv_counts = P->recv_counts;
+  D->offsets = P->offsets;
   cudaGetDevice(&D->device);
   const size_t vs = dtype_size(dtype);
   int s = PJDS_OK;
@@ -377,37 +415,70 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
   std::vector<int32_t> p2p_ids;
   std::vector<int64_t> p2p_seg;
   try {
-    // ---- the two pJDS parts
-    std::vector<uint8_t> v_loc(P->loc_src.size() * vs), v_nl(P->nl_src.size() * vs);
-    const uint8_t* vin = (const uint8_t*)val;
-    for (size_t k = 0; k < P->loc_src.size(); ++k) std::memcpy(&v_loc[k * vs], vin + P->loc_src[k] * vs, vs);
-    for (size_t k = 0; k < P->nl_src.size(); ++k) std::memcpy(&v_nl[k * vs], vin + P->nl_src[k] * vs, vs);
-    D->A_loc = new pjds_mat();
-    s = convert_pjds(D->A_loc->h, P->n_loc, P->n_loc, P->loc_rowptr.data(), P->loc_col.data(), v_loc.data(), dtype,
-                     block_rows, sym);
-    if (s != PJDS_OK) return fail(s);  // (perm is not filled on failure)
-    // local inverse permutation (permuted basis: local row i lives at position inv[i])
-    std::vector<int32_t> inv;
-    if (sym) {
-      inv.resize(P->n_loc);
-      for (int64_t k = 0; k < P->n_loc; ++k) inv[D->A_loc->h.perm[k]] = (int32_t)k;
-      D->A_loc->direct_store = true;
-      D->A_loc->flags = PJDS_PERM_SYMMETRIC;
-    }
-    if ((s = upload_pjds(D->A_loc, nullptr)) != PJDS_OK) return fail(s);
-    D->A_loc->ncols = P->n_loc;
-    const int64_t m = (int64_t)P->rows_nl.size();
-    if (m > 0) {
-      D->A_nl = new pjds_mat();
-      s = convert_pjds(D->A_nl->h, m, std::max<int64_t>(D->halo, 1), P->nl_rowptr.data(), P->nl_col.data(),
-                       v_nl.data(), dtype, block_rows, false);
-      // store to local row rows_nl[perm_nl[k]] (or its position in the local permuted basis)
-      std::vector<int32_t> map(P->rows_nl);
-      if (sym)
-        for (auto& r : map) r = inv[r];
-      if (s == PJDS_OK) s = upload_pjds(D->A_nl, map.data());
+    std::vector<int32_t> inv;  // local inverse permutation (permuted basis: row i at position inv[i])
+    if (transport == PJDS_TRANSPORT_DIRECT) {
+      // ---- one pJDS matrix over the full local rows (CRS order kept within each row); columns
+      // stay temporary codes until pjds_dist_direct_connect knows the owners' window positions:
+      // local column c -> c, halo slot h -> n_loc + h
+      int shift = 0;
+      int64_t maxn = 1;
+      for (int q = 0; q < R; ++q) maxn = std::max(maxn, P->offsets[q + 1] - P->offsets[q]);
+      while ((int64_t(1) << shift) < maxn) ++shift;
+      if (R > kWinTable || ((int64_t)R << shift) > (int64_t(1) << 31))
+        return fail(set_error(PJDS_ERR_UNSUPPORTED, "DIRECT transport: needs nranks <= 64 and "
+                                                    "nranks * 2^ceil(log2(max rows per rank)) <= 2^31"));
+      D->win_shift = shift;
+      const int64_t nl = P->n_loc;
+      std::vector<int64_t> frp(nl + 1, 0);
+      std::vector<int32_t> nl_len(nl, 0);
+      for (int64_t a = 0; a < (int64_t)P->rows_nl.size(); ++a)
+        nl_len[P->rows_nl[a]] = (int32_t)(P->nl_rowptr[a + 1] - P->nl_rowptr[a]);
+      for (int64_t i = 0; i < nl; ++i) frp[i + 1] = frp[i] + (P->loc_rowptr[i + 1] - P->loc_rowptr[i]) + nl_len[i];
+      std::vector<int32_t> fcol(P->nnz_loc);
+      for (size_t k = 0; k < P->loc_src.size(); ++k) fcol[P->loc_src[k]] = P->loc_col[k];
+      for (size_t k = 0; k < P->nl_src.size(); ++k) fcol[P->nl_src[k]] = (int32_t)(nl + P->nl_col[k]);
+      D->A_loc = new pjds_mat();
+      s = convert_pjds(D->A_loc->h, nl, nl + D->halo, frp.data(), fcol.data(), val, dtype, block_rows, false);
       if (s != PJDS_OK) return fail(s);
-      D->A_nl->ncols = D->halo;
+      if (sym) {
+        inv.resize(nl);
+        for (int64_t k = 0; k < nl; ++k) inv[D->A_loc->h.perm[k]] = (int32_t)k;
+        D->A_loc->direct_store = true;
+        D->A_loc->flags = PJDS_PERM_SYMMETRIC;
+      }
+      D->A_loc->ncols = nl + D->halo;
+    } else {
+      // ---- the two pJDS parts
+      std::vector<uint8_t> v_loc(P->loc_src.size() * vs), v_nl(P->nl_src.size() * vs);
+      const uint8_t* vin = (const uint8_t*)val;
+      for (size_t k = 0; k < P->loc_src.size(); ++k) std::memcpy(&v_loc[k * vs], vin + P->loc_src[k] * vs, vs);
+      for (size_t k = 0; k < P->nl_src.size(); ++k) std::memcpy(&v_nl[k * vs], vin + P->nl_src[k] * vs, vs);
+      D->A_loc = new pjds_mat();
+      s = convert_pjds(D->A_loc->h, P->n_loc, P->n_loc, P->loc_rowptr.data(), P->loc_col.data(), v_loc.data(), dtype,
+                       block_rows, sym);
+      if (s != PJDS_OK) return fail(s);  // (perm is not filled on failure)
+      // local inverse permutation (permuted basis: local row i lives at position inv[i])
+      if (sym) {
+        inv.resize(P->n_loc);
+        for (int64_t k = 0; k < P->n_loc; ++k) inv[D->A_loc->h.perm[k]] = (int32_t)k;
+        D->A_loc->direct_store = true;
+        D->A_loc->flags = PJDS_PERM_SYMMETRIC;
+      }
+      if ((s = upload_pjds(D->A_loc, nullptr)) != PJDS_OK) return fail(s);
+      D->A_loc->ncols = P->n_loc;
+      const int64_t m = (int64_t)P->rows_nl.size();
+      if (m > 0) {
+        D->A_nl = new pjds_mat();
+        s = convert_pjds(D->A_nl->h, m, std::max<int64_t>(D->halo, 1), P->nl_rowptr.data(), P->nl_col.data(),
+                         v_nl.data(), dtype, block_rows, false);
+        // store to local row rows_nl[perm_nl[k]] (or its position in the local permuted basis)
+        std::vector<int32_t> map(P->rows_nl);
+        if (sym)
+          for (auto& r : map) r = inv[r];
+        if (s == PJDS_OK) s = upload_pjds(D->A_nl, map.data());
+        if (s != PJDS_OK) return fail(s);
+        D->A_nl->ncols = D->halo;
+      }
     }
     D->permuted = sym;
     // ---- send schedule
@@ -421,6 +492,16 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       if (sym)
         for (auto& v : ids) v = inv[v];  // gather from x in the local permuted basis
       pos += cnt;
+      if (transport == PJDS_TRANSPORT_DIRECT) {  // q reads these window positions itself
+        D->dir_send_pos.insert(D->dir_send_pos.end(), ids.begin(), ids.end());
+        D->send_peers.push_back(q);
+        pjds_dist::PeerSend ps;
+        ps.peer = q;
+        ps.packed = false;
+        ps.runs = {{0, cnt}};
+        D->sends.push_back(std::move(ps));
+        continue;
+      }
       if (transport == PJDS_TRANSPORT_P2P) {  // every entry is gathered by the fused pack+put kernel
         p2p_ids.insert(p2p_ids.end(), ids.begin(), ids.end());
         p2p_seg.push_back((int64_t)p2p_ids.size());
@@ -453,6 +534,12 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       auto runs = runs_of(P->recv_cols.data() + hoff, cnt);
       pjds_dist::PeerRecv pr;
       pr.peer = q;
+      if (transport == PJDS_TRANSPORT_DIRECT) {  // no messages: read in place from q's window
+        pr.runs = {{hoff, cnt}};
+        D->recvs.push_back(std::move(pr));
+        hoff += cnt;
+        continue;
+      }
       if (!sym && (int)runs.size() <= kMaxRuns) {  // permuted basis: one packed message per peer
         int64_t o = hoff;
         for (auto& r : runs) {
@@ -472,6 +559,8 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
   // ---- device buffers, streams, transport
   if (transport == PJDS_TRANSPORT_P2P) {
     if ((s = p2p_setup(D, p2p_ids, p2p_seg)) != PJDS_OK) return fail(s);
+  } else if (transport == PJDS_TRANSPORT_DIRECT) {
+    if ((s = direct_setup(D)) != PJDS_OK) return fail(s);
   } else if (cudaMalloc(&D->d_halo, std::max<size_t>(D->halo * vs, 16)) != cudaSuccess) {
     return fail(set_error(PJDS_ERR_OOM, "halo allocation failed"));
   }
@@ -514,6 +603,7 @@ int pjds_dist_destroy(pjds_dist_t D) {
   cudaFree(D->p2p_region); cudaFree(D->d_p2p_idx); cudaFree(D->d_p2p_seg);
   cudaFree(D->d_send_peers); cudaFree(D->d_recv_peers);
   cudaFree(D->d_dst[0]); cudaFree(D->d_dst[1]); cudaFree(D->d_ready_targets); cudaFree(D->d_done_targets);
+  cudaFree(D->d_win);
   pjds_destroy(D->A_loc);
   pjds_destroy(D->A_nl);
   delete D;
@@ -522,7 +612,8 @@ int pjds_dist_destroy(pjds_dist_t D) {
 
 int pjds_dist_p2p_export(pjds_dist_t D, void* blob, int64_t* bytes) {
   if (!D || !bytes) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_export: NULL argument");
-  if (D->transport != PJDS_TRANSPORT_P2P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_export: not a P2P handle");
+  if (D->transport != PJDS_TRANSPORT_P2P && D->transport != PJDS_TRANSPORT_DIRECT)
+    return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_export: not a P2P / DIRECT handle");
   if (D->R > kP2PMaxRanks) return set_error(PJDS_ERR_UNSUPPORTED, "P2P transport supports at most 64 ranks");
   *bytes = (int64_t)sizeof(P2PBlob);
   if (!blob) return PJDS_OK;
@@ -530,6 +621,7 @@ int pjds_dist_p2p_export(pjds_dist_t D, void* blob, int64_t* bytes) {
   std::memset(&b, 0, sizeof(b));
   PJDS_CUDA_TRY(cudaIpcGetMemHandle(&b.handle, D->p2p_region));
   b.halo_bytes = D->p2p_halo_bytes;
+  b.flags_off = D->p2p_flags_off;
   b.R = D->R;
   b.rank = D->rank;
   for (int q = 0; q < D->R; ++q) b.recv_off[q] = D->recv_off[q];
@@ -564,12 +656,12 @@ int pjds_dist_p2p_connect(pjds_dist_t D, const void* blobs, int64_t blob_bytes) 
     const size_t off = (size_t)b[q].recv_off[D->rank] * vs;
     dst0.push_back(base + off);
     dst1.push_back(base + b[q].halo_bytes + off);
-    ready_t.push_back((uint64_t*)(base + 2 * b[q].halo_bytes) + D->rank);
+    ready_t.push_back((uint64_t*)(base + b[q].flags_off) + D->rank);
   }
   for (int p : D->recv_peers) {  // tell p when I am done reading its data
     PJDS_TRY(open(p));
     char* base = (char*)D->peer_regions[p];
-    done_t.push_back((uint64_t*)(base + 2 * b[p].halo_bytes) + D->R + D->rank);
+    done_t.push_back((uint64_t*)(base + b[p].flags_off) + D->R + D->rank);
   }
   if (!dst0.empty()) {
     PJDS_CUDA_TRY(cudaMemcpy(D->d_dst[0], dst0.data(), dst0.size() * sizeof(void*), cudaMemcpyHostToDevice));
@@ -582,9 +674,93 @@ int pjds_dist_p2p_connect(pjds_dist_t D, const void* blobs, int64_t blob_bytes) 
   return PJDS_OK;
 }
 
+int pjds_dist_x_window(pjds_dist_t D, void** x_window) {
+  if (!D || !x_window) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_x_window: NULL argument");
+  if (D->transport != PJDS_TRANSPORT_DIRECT) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_x_window: not a DIRECT handle");
+  *x_window = D->p2p_region;
+  return PJDS_OK;
+}
+
+int pjds_dist_direct_positions(pjds_dist_t D, int32_t* pos) {
+  if (!D) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_positions: NULL handle");
+  if (D->transport != PJDS_TRANSPORT_DIRECT) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_positions: not a DIRECT handle");
+  if (!D->dir_send_pos.empty()) {
+    if (!pos) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_positions: NULL pos");
+    std::memcpy(pos, D->dir_send_pos.data(), D->dir_send_pos.size() * 4);
+  }
+  return PJDS_OK;
+}
+
+int pjds_dist_direct_connect(pjds_dist_t D, const int32_t* halo_pos, const void* blobs, int64_t blob_bytes) {
+  if (!D || !blobs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: NULL argument");
+  if (D->transport != PJDS_TRANSPORT_DIRECT) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: not a DIRECT handle");
+  if (D->p2p_connected) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: already connected");
+  if (D->halo > 0 && !halo_pos) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: NULL halo_pos");
+  if (blob_bytes != (int64_t)sizeof(P2PBlob)) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: blob size");
+  const P2PBlob* b = (const P2PBlob*)blobs;
+  for (int q = 0; q < D->R; ++q)
+    if (b[q].R != D->R || b[q].rank != q) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: blobs not rank-ordered");
+  // halo slot -> owner; every position must lie inside the owner's window
+  std::vector<int32_t> owner(D->halo);
+  for (int q = 0, h = 0; q < D->R; ++q)
+    for (int64_t i = 0; i < D->recv_counts[q]; ++i, ++h) {
+      owner[h] = q;
+      if (halo_pos[h] < 0 || halo_pos[h] >= D->offsets[q + 1] - D->offsets[q])
+        return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: halo position outside the owner's rows");
+    }
+  auto open = [&](int q) -> int {
+    if (q == D->rank || D->peer_regions[q]) return PJDS_OK;
+    void* p = nullptr;
+    PJDS_CUDA_TRY(cudaIpcOpenMemHandle(&p, b[q].handle, cudaIpcMemLazyEnablePeerAccess));
+    D->peer_regions[q] = p;
+    return PJDS_OK;
+  };
+  std::vector<void*> bases(kWinTable, nullptr);
+  std::vector<uint64_t*> ready_t, done_t;
+  bases[D->rank] = D->p2p_region;
+  for (int q : D->send_peers) {  // q reads my window: tell q when it holds this call's x
+    PJDS_TRY(open(q));
+    ready_t.push_back((uint64_t*)((char*)D->peer_regions[q] + b[q].flags_off) + D->rank);
+  }
+  for (int p : D->recv_peers) {  // I read p's window: tell p when I am done with it
+    PJDS_TRY(open(p));
+    bases[p] = D->peer_regions[p];
+    done_t.push_back((uint64_t*)((char*)D->peer_regions[p] + b[p].flags_off) + D->R + D->rank);
+  }
+  PJDS_CUDA_TRY(cudaMemcpy(D->d_win, bases.data(), kWinTable * sizeof(void*), cudaMemcpyHostToDevice));
+  if (!ready_t.empty())
+    PJDS_CUDA_TRY(cudaMemcpy(D->d_ready_targets, ready_t.data(), ready_t.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  if (!done_t.empty())
+    PJDS_CUDA_TRY(cudaMemcpy(D->d_done_targets, done_t.data(), done_t.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  // final column codes (owner << shift) | window position, then upload
+  pjds_mat* A = D->A_loc;
+  auto& h = A->h;
+  const int64_t nl = D->n_loc;
+  const int sh = D->win_shift;
+  std::vector<int32_t> inv(nl);
+  for (int64_t k = 0; k < nl; ++k) inv[h.perm[k]] = D->permuted ? (int32_t)k : h.perm[k];
+  const int32_t me = D->rank << sh;
+#pragma omp parallel for
+  for (int64_t k = 0; k < (int64_t)h.col.size(); ++k) {
+    const int32_t c = h.col[k];
+    if (c < nl) {
+      h.col[k] = me | inv[c];
+    } else {
+      const int64_t hs = c - nl;
+      h.col[k] = (owner[hs] << sh) | halo_pos[hs];
+    }
+  }
+  int s = upload_pjds(A, nullptr);
+  if (s != PJDS_OK) return s;
+  A->d_win = D->d_win;
+  A->win_shift = sh;
+  D->p2p_connected = true;
+  return PJDS_OK;
+}
+
 int pjds_dist_p2p_check(pjds_dist_t D, int32_t* timed_out) {
   if (!D || !timed_out) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_p2p_check: NULL argument");
-  if (D->transport != PJDS_TRANSPORT_P2P) {
+  if (D->transport != PJDS_TRANSPORT_P2P && D->transport != PJDS_TRANSPORT_DIRECT) {
     *timed_out = 0;
     return PJDS_OK;
   }
@@ -647,6 +823,31 @@ int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t
     if (tr) PJDS_CUDA_TRY(cudaEventRecord(D->tev[i], st));
     return PJDS_OK;
   };
+  if (D->transport == PJDS_TRANSPORT_DIRECT) {
+    // x into this rank's window (skipped when the caller computed it there), "ready" to the
+    // ranks that read it, wait for the owners I read, ONE kernel over all local rows, then
+    // "done" to the owners and wait until every reader of my window is done (x reusable after)
+    if (!D->p2p_connected) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: call pjds_dist_direct_connect first");
+    if (y == (void*)D->p2p_region && D->n_loc > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: y aliases the x window");
+    const uint64_t sq = ++D->seq;
+    const int ns = (int)D->send_peers.size(), nr = (int)D->recv_peers.size();
+    PJDS_TRY(mark(0, s));
+    PJDS_TRY(mark(1, s));
+    if (x != (const void*)D->p2p_region && D->n_loc > 0)
+      PJDS_CUDA_TRY(cudaMemcpyAsync(D->p2p_region, x, D->n_loc * vsz(D), cudaMemcpyDeviceToDevice, s));
+    PJDS_TRY(mark(2, s));
+    PJDS_TRY(p2p_launch_signal(D->d_ready_targets, ns, sq, s));
+    PJDS_TRY(p2p_launch_wait(D->ready_flags(), D->d_recv_peers, nr, sq, D->err_flag(), s));
+    PJDS_TRY(mark(3, s));
+    PJDS_TRY(launch_pjds_spmv(D->A_loc, y, D->p2p_region, s, false));
+    PJDS_TRY(mark(4, s));
+    PJDS_TRY(mark(5, s));
+    PJDS_TRY(p2p_launch_signal(D->d_done_targets, nr, sq, s));
+    PJDS_TRY(p2p_launch_wait(D->done_flags(), D->d_send_peers, ns, sq, D->err_flag(), s));
+    PJDS_TRY(mark(6, s));
+    D->traced = D->traced || tr;
+    return PJDS_OK;
+  }
   if (!comm_needed) {  // R = 1 or no halo: local part only (+ empty nonlocal)
     for (int i = 0; i < 4; ++i) PJDS_TRY(mark(i, s));
     PJDS_TRY(launch_pjds_spmv(D->A_loc, y, x, s, false));

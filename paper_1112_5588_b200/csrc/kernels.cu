@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 #include <vector>
 #include "internal.h"
 
@@ -93,6 +94,15 @@ __device__ __forceinline__ float ld_rhs(const float* p, uint64_t pol) {
   asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
+// RHS gather of the fused remote-gather dist kernel (PJDS_TRANSPORT_DIRECT): column code
+// (owner << shift) | position addresses owner's x window (own memory, or a peer's through its
+// CUDA-IPC mapping -- an NVLink load between GPUs); otherwise a plain x[c] gather
+constexpr int kMaxWin = 64;
+template <bool WIN, typename T>
+__device__ __forceinline__ T gather_x(const T* x, const T* const* win, int shift, int c, uint64_t pol) {
+  if constexpr (WIN) return ld_rhs(win[(unsigned)c >> shift] + (c & ((1 << shift) - 1)), pol);
+  else return ld_rhs(x + c, pol);
+}
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
@@ -163,13 +173,18 @@ enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 
 // PIPE: software-pipelined main loop (next chunk's val/col loads in flight during the current
 // chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
-template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false>
+// WIN: fused remote-gather dist kernel (x = the owners' windows, see gather_x).
+template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false, bool WIN = false>
 __global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
-                 double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off) {
+                 double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off,
+                 const T* const* __restrict__ win, int win_shift) {
   __shared__ Off s_cs[kSmemCS];
+  __shared__ const T* s_win[WIN ? kMaxWin : 1];
+  if constexpr (WIN)
+    for (int i = threadIdx.x; i < kMaxWin; i += kThreads) s_win[i] = win[i];
   // execution order of the CTA tiles (storage order, or by original row; results are identical)
   const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
   const int64_t t = tile * kThreads + threadIdx.x;
@@ -212,7 +227,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int r = 0; r < R; ++r) xv[u][r] = ld_rhs(x + ca[u].v[r], pol_x);
+        for (int r = 0; r < R; ++r) xv[u][r] = gather_x<WIN>(x, s_win, win_shift, ca[u].v[r], pol_x);
       const int jn = j + U;
       const bool more = jn + U <= len;
       Vec<T, R> vb[U];
@@ -251,7 +266,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int r = 0; r < R; ++r) xv[u][r] = ld_rhs(x + c[u].v[r], pol_x);
+      for (int r = 0; r < R; ++r) xv[u][r] = gather_x<WIN>(x, s_win, win_shift, c[u].v[r], pol_x);
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -272,7 +287,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
     for (int u = 0; u < U; ++u)
       if (j + u < len)
 #pragma unroll
-        for (int r = 0; r < R; ++r) xv[u][r] = ld_rhs(x + c[u].v[r], pol_x);
+        for (int r = 0; r < R; ++r) xv[u][r] = gather_x<WIN>(x, s_win, win_shift, c[u].v[r], pol_x);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (j + u < len)
@@ -436,10 +451,23 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
                       (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
                        (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(A, R, &order));
-#define PJDS_LAUNCH_PF(M, PF, IL)                                                                        \
-  pjds_spmv_kernel<T, Off, R, U, M, PF, IL><<<(unsigned)grid, kThreads, 0, s>>>(                        \
+#define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
+  pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part, h.sigma, \
-      A->d_wcs_off)
+      A->d_wcs_off, (const T* const*)A->d_win, A->win_shift)
+#define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
+  if (A->d_win) {  // fused remote-gather dist matrix: plain main loop, direct or perm store
+    if constexpr (std::is_same<Off, int32_t>::value) {
+      if (mode == STORE_DIRECT) PJDS_LAUNCH_W(STORE_DIRECT, false, false, true);
+      else if (mode == STORE_PERM) PJDS_LAUNCH_W(STORE_PERM, false, false, true);
+      else return set_error(PJDS_ERR_UNSUPPORTED, "window matrices support y = A x only");
+      count_launch();
+      PJDS_CUDA_TRY(cudaGetLastError());
+      return PJDS_OK;
+    } else {
+      return set_error(PJDS_ERR_UNSUPPORTED, "window matrices need 32-bit jagged offsets");
+    }
+  }
   const bool il = g_il && R > 1 && h.br % (32 * R) == 0;
 #define PJDS_LAUNCH(M)                    \
   if (pipe) PJDS_LAUNCH_PF(M, true, false); \
@@ -456,6 +484,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   }
 #undef PJDS_LAUNCH
 #undef PJDS_LAUNCH_PF
+#undef PJDS_LAUNCH_W
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;
@@ -490,8 +519,8 @@ static bool g_force_off64 = false;  // test hook: exercise the 64-bit offset ker
 template <typename T, typename Off>
 int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, int mode, double* dp, int64_t* np) {
   int R = g_var_r, U = g_var_u;
-  bool pipe = g_pipe;
-  if (g_split) {
+  bool pipe = g_pipe && !A->d_win;
+  if (g_split && !A->d_win) {
     T* yy = (T*)y;
     const T* xx = (const T*)x;
     if (g_split == 2) return U >= 8 ? launch_pjds_split_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np)

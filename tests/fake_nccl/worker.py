@@ -30,6 +30,8 @@ offs = np.array([(nb * r // R) * seg for r in range(R + 1)], np.int64)
 lo, hi = offs[rank], offs[rank + 1]
 x = inputs.vector(n)
 out = {}
+# DIRECT: one kernel over the unsplit rows -> bitwise the plain FMA chain; others: the split rule
+chain = oracle.spmv_chain(n, rp, col, val, x) if transport == "direct" else None
 for permuted in (False, True):
     try:
         D = pj.DistPjds.create(n, offs, rp[lo:hi + 1] - rp[lo], col[rp[lo]:rp[hi]], val[rp[lo]:rp[hi]],
@@ -40,16 +42,20 @@ for permuted in (False, True):
     if permuted:
         xt = D.to_permuted(torch.empty_like(xt), xt)
     for no in (False, True):
+        xin = xt
+        if transport == "direct" and no:  # x computed in the exported window: no per-call copy
+            xin = D.x_window()
+            xin.copy_(xt)
         y = torch.full_like(xt, float("nan"))
         for _ in range(reps):  # several calls: exercises the double-buffered halo / flag sequence
-            D.spmv(y, xt, no_overlap=no, trace=True)
+            D.spmv(y, xin, no_overlap=no, trace=True)
         if permuted:
             y = D.from_permuted(torch.empty_like(y), y)
         torch.cuda.synchronize()
         ys = [None] * R
         dist.all_gather_object(ys, y.cpu().numpy())
         yall = np.concatenate(ys)
-        ref = odist.spmv(odist.split(n, rp, col, val, offs), x) if name != "C3" else None
+        ref = chain if chain is not None else (odist.spmv(odist.split(n, rp, col, val, offs), x) if name != "C3" else None)
         yl, b = oracle.spmv_ld(n, rp, col, val, x)
         ok = bool(oracle.acceptance(yall, yl, b, np.diff(rp), np.float64).all())
         out[f"perm{int(permuted)}_noov{int(no)}"] = {"o2": ok, "bitwise_vs_split_oracle": bool(np.array_equal(yall, ref)) if ref is not None else None,
