@@ -836,14 +836,14 @@ int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t
     if (x != (const void*)D->p2p_region && D->n_loc > 0)
       PJDS_CUDA_TRY(cudaMemcpyAsync(D->p2p_region, x, D->n_loc * vsz(D), cudaMemcpyDeviceToDevice, s));
     PJDS_TRY(mark(2, s));
-    PJDS_TRY(p2p_launch_signal(D->d_ready_targets, ns, sq, s));
-    PJDS_TRY(p2p_launch_wait(D->ready_flags(), D->d_recv_peers, nr, sq, D->err_flag(), s));
+    PJDS_TRY(p2p_launch_signal_wait(D->d_ready_targets, ns, sq, D->ready_flags(), D->d_recv_peers, nr, sq,
+                                    D->err_flag(), s));
     PJDS_TRY(mark(3, s));
     PJDS_TRY(launch_pjds_spmv(D->A_loc, y, D->p2p_region, s, false));
     PJDS_TRY(mark(4, s));
     PJDS_TRY(mark(5, s));
-    PJDS_TRY(p2p_launch_signal(D->d_done_targets, nr, sq, s));
-    PJDS_TRY(p2p_launch_wait(D->done_flags(), D->d_send_peers, ns, sq, D->err_flag(), s));
+    PJDS_TRY(p2p_launch_signal_wait(D->d_done_targets, nr, sq, D->done_flags(), D->d_send_peers, ns, sq,
+                                    D->err_flag(), s));
     PJDS_TRY(mark(6, s));
     D->traced = D->traced || tr;
     return PJDS_OK;

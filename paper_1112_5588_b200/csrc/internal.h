@@ -111,6 +111,8 @@ int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t
 // P2P transport kernels (p2p.cu)
 int p2p_launch_wait(const uint64_t* flags, const int* peers, int np, uint64_t target, unsigned* err, cudaStream_t s);
 int p2p_launch_signal(uint64_t* const* targets, int nt, uint64_t value, cudaStream_t s);
+int p2p_launch_signal_wait(uint64_t* const* targets, int nt, uint64_t value, const uint64_t* flags, const int* peers,
+                           int np, uint64_t target, unsigned* err, cudaStream_t s);
 int p2p_launch_pack_put(const void* x, const int* idx, const int64_t* seg, void* const* dst, int npeers,
                         int64_t max_count, int dtype, cudaStream_t s);
 int launch_ellr_spmv(const ellr_mat* A, void* y, const void* x, cudaStream_t s);

@@ -94,13 +94,25 @@ __device__ __forceinline__ float ld_rhs(const float* p, uint64_t pol) {
   asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
+// window gathers use the plain (coherent) global load, L1-allocating: the windows include peer
+// memory mapped over NVLink, for which the plain load is the conservative choice
+__device__ __forceinline__ double ld_win(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_win(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
 // RHS gather of the fused remote-gather dist kernel (PJDS_TRANSPORT_DIRECT): column code
 // (owner << shift) | position addresses owner's x window (own memory, or a peer's through its
 // CUDA-IPC mapping -- an NVLink load between GPUs); otherwise a plain x[c] gather
 constexpr int kMaxWin = 64;
 template <bool WIN, typename T>
 __device__ __forceinline__ T gather_x(const T* x, const T* const* win, int shift, int c, uint64_t pol) {
-  if constexpr (WIN) return ld_rhs(win[(unsigned)c >> shift] + (c & ((1 << shift) - 1)), pol);
+  if constexpr (WIN) return ld_win(win[(unsigned)c >> shift] + (c & ((1 << shift) - 1)), pol);
   else return ld_rhs(x + c, pol);
 }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }

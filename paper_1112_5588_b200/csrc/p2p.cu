@@ -12,6 +12,9 @@
 //                   A_nl on halo buffer s%2 ; signal done[r] = s at every sender p
 // Signals are system-scope release stores after __threadfence_system(); waits are acquire loads
 // with a bounded spin (the err word records a timeout instead of hanging the GPU).
+// The DIRECT transport (dist.cpp) reuses the flags with p2p_signal_wait_kernel: "my x window holds
+// call s" out + the owners' "ready" in before its kernel, "done reading" out + the readers' "done"
+// in after it.
 #include <algorithm>
 #include <cstring>
 #include "internal.h"
@@ -49,6 +52,28 @@ __global__ void p2p_signal_kernel(uint64_t* const* targets, int nt, uint64_t val
   for (int i = 0; i < nt; ++i) st_release_sys(targets[i], value);
 }
 
+// signal, then wait, in one launch (DIRECT transport: "ready" out / owners' "ready" in, and
+// "done" out / readers' "done" in)
+__global__ void p2p_signal_wait_kernel(uint64_t* const* targets, int nt, uint64_t value, const uint64_t* flags,
+                                       const int* peers, int np, uint64_t target, unsigned* err) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < nt; ++i) st_release_sys(targets[i], value);
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  if (i >= np) return;
+  const uint64_t* f = flags + peers[i];
+  const long long t0 = clock64();
+  while (ld_acquire_sys(f) < target) {
+    if (clock64() - t0 > 20000000000LL) {
+      atomicExch(err, 1u);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
 // blockIdx.y = send peer; entries [seg[p], seg[p+1]) of idx go to dst[p][0 .. count)
 template <typename T>
 __global__ void p2p_pack_put_kernel(const T* __restrict__ x, const int* __restrict__ idx,
@@ -73,6 +98,15 @@ int p2p_launch_wait(const uint64_t* flags, const int* peers, int np, uint64_t ta
 int p2p_launch_signal(uint64_t* const* targets, int nt, uint64_t value, cudaStream_t s) {
   if (nt <= 0) return PJDS_OK;
   p2p_signal_kernel<<<1, 32, 0, s>>>(targets, nt, value);
+  count_launch();
+  PJDS_CUDA_TRY(cudaGetLastError());
+  return PJDS_OK;
+}
+
+int p2p_launch_signal_wait(uint64_t* const* targets, int nt, uint64_t value, const uint64_t* flags, const int* peers,
+                           int np, uint64_t target, unsigned* err, cudaStream_t s) {
+  if (nt <= 0 && np <= 0) return PJDS_OK;
+  p2p_signal_wait_kernel<<<1, 64, 0, s>>>(targets, nt, value, flags, peers, np, target, err);
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;
