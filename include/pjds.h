@@ -339,7 +339,9 @@ int pjds_dist_stats(pjds_dist_t D, pjds_dist_info_t* out, int64_t* recv_per_peer
    [3] NCCL exchange, [4] compute stream waiting for the exchange, [5] nonlocal part.
    INVALID_ARG if no traced call was made. */
 int pjds_dist_trace(pjds_dist_t D, double* ms /* [6] */);
-/* The two pJDS parts (owned by D; do not destroy): A_loc, A_nl (A_nl may be NULL if empty). */
+/* The two pJDS parts (owned by D; do not destroy): A_loc, A_nl (A_nl may be NULL if empty).
+   DIRECT handles: A_loc = the one matrix over the full local rows (its spmv gathers from the x
+   windows, whatever x pointer is passed), A_nl = NULL. */
 int pjds_dist_parts(pjds_dist_t D, pjds_t* A_loc, pjds_t* A_nl);
 /* Frees the handle (and, for NCCL, the communicator; for P2P, the IPC mappings and the exported
    region).  Collective in effect: synchronise all ranks' streams and barrier before destroying, so
