@@ -156,18 +156,39 @@ def _allreduce(dist, t, op):
 def time_oracle(n, rp, col, val, x, budget_s: float, max_reps: int, min_reps: int = 1, threads: int = 0,
                 warmup: int = 1):
     """The oracle's plain CRS loop (oracle_spmv_crs: OpenMP static over rows, all visible cores or
-    `threads`), repeated until the time budget is spent.  Returns (median s per product, reps, cores, total s)."""
+    `threads`), repeated until the time budget is spent.  Returns (median s per product, reps, cores,
+    total s, y of the warm-up product)."""
     import oracle
     cores = threads or len(os.sched_getaffinity(0))
     for _ in range(max(warmup, 1)):
-        oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)
+        y_cpu = oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)
     ts = []
     t_end = time.perf_counter() + budget_s
     while (time.perf_counter() < t_end and len(ts) < max_reps) or len(ts) < min_reps:
         t0 = time.perf_counter()
         oracle.spmv_crs(n, rp, col, val, x, nthreads=cores)
         ts.append(time.perf_counter() - t0)
-    return float(np.median(ts)), len(ts), cores, float(sum(ts))
+    return float(np.median(ts)), len(ts), cores, float(sum(ts)), y_cpu
+
+
+def parity_vs_cpu(y_gpu, y_cpu, rp, col, val, x, rows):
+    """SURVEY §8(d) step 6, parity in the same run: sampled rows of the GPU product against the
+    cpu_baseline leg's own product on the same inputs.  Both are O2-bounded approximations of the
+    exact row sum, so |y_gpu - y_cpu| <= 2 * 4 nnz_i eps sum_j |a_ij x_j| (triangle inequality)."""
+    lens = (rp[rows + 1] - rp[rows]).astype(np.int64)
+    idx = np.repeat(rp[rows], lens) + (np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens))
+    bound = np.zeros(len(rows))
+    np.add.at(bound, np.repeat(np.arange(len(rows)), lens), np.abs(val[idx].astype(np.float64) * x[col[idx]]))
+    eps = np.finfo(val.dtype).eps
+    diff = np.abs(y_gpu[rows].astype(np.float64) - y_cpu[rows].astype(np.float64))
+    tol = 8.0 * lens * eps * bound * (1 + 1e-6)
+    ok = (diff <= tol) & np.isfinite(y_gpu[rows])
+    rel = diff / np.maximum(bound, np.finfo(np.float64).tiny)
+    return {"rows_checked": int(len(rows)), "within_bound": bool(ok.all()), "rows_outside": int((~ok).sum()),
+            "max_err_over_sum_abs": float(rel.max()) if len(rows) else 0.0,
+            "bound": "|y_gpu - y_cpu| <= 8 nnz_i eps sum_j |a_ij x_j| (both O2-bounded)",
+            "reference": "the cpu_baseline leg's oracle_spmv_crs product on the same inputs",
+            "gpu_finite_all_rows": bool(np.isfinite(y_gpu).all())}
 
 
 # ------------------------------------------------------------------------------------------ main
@@ -248,11 +269,11 @@ def main():
     # CPU oracle baseline on the same matrix (rank 0, N=1 only), bounded to ~10 s
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        t, reps, cores, tot = time_oracle(n, rp, col, val, x_host, budget_s=10.0, max_reps=200)
+        t, reps, cores, tot, y_cpu = time_oracle(n, rp, col, val, x_host, budget_s=10.0, max_reps=200)
         cpu = {"value": round(2.0 * nnz_loc / t / 1e9, 3), "unit": "GFlop/s", "cores": cores, "kind": "oracle",
                "sample": f"whole {a.config} matrix ({nnz_loc} nnz), {reps} products, median; {tot:.1f} s of "
                          f"oracle_spmv_crs ({np.dtype(npdt).name}, OpenMP {cores} threads)"}
-        t1, reps1, _, _ = time_oracle(n, rp, col, val, x_host, budget_s=3.0, max_reps=3, threads=1)
+        t1, reps1, _, _, _ = time_oracle(n, rp, col, val, x_host, budget_s=3.0, max_reps=3, threads=1)
         cpu["single_thread"] = {"value": round(2.0 * nnz_loc / t1 / 1e9, 3), "reps": reps1}
     nnz = nnz_loc
     if use_dist:
@@ -325,6 +346,16 @@ def main():
         tr = tv.tolist()
     trials = {"n": 5, "steps_each": kt, "median_ms": round(float(np.median(tr)), 5), "best_ms": round(min(tr), 5),
               "best_gflops": round(2.0 * nnz / (min(tr) * 1e-3) / 1e9, 2)}
+    parity = None
+    if cpu is not None:  # same-run parity against the cpu_baseline leg's product
+        yo = y
+        if permuted:
+            yo = torch.empty_like(y)
+            A.from_permuted(yo, y)
+        y_gpu_host = yo.cpu().numpy()
+        rows = np.unique(np.concatenate([np.random.default_rng(7).integers(0, n, 100000), [0, n - 1]]))
+        parity = parity_vs_cpu(y_gpu_host, y_cpu, rp, col, val, x_host, rows)
+        del y_gpu_host, y_cpu
     dist_info = None
     if use_dist:
         # vector mode (exchange, then compute) as the reference point for "communication hidden",
@@ -516,6 +547,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "parity": parity,
             "footprint": footprint,
             "compare": compare or None,
             "dist": dist_info,
@@ -538,7 +570,7 @@ def reference_arm(a, world, npdt):
     x = inputs.vector(g.n, npdt)
     nnz = int(rp[-1])
     w = max(a.warmup, 3)
-    t, reps, cores, tot = time_oracle(g.n, rp, col, val, x, budget_s=120.0, max_reps=a.steps, warmup=w)
+    t, reps, cores, tot, _ = time_oracle(g.n, rp, col, val, x, budget_s=120.0, max_reps=a.steps, warmup=w)
     v = 2.0 * nnz / t / 1e9
     sample = f"whole {a.config} matrix ({nnz} nnz) per step, {reps} steps (median), oracle_spmv_crs"
     print(json.dumps({
