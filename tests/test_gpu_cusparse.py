@@ -22,7 +22,8 @@ import pytest
 import inputs
 import oracle
 
-pytestmark = [pytest.mark.gpu, pytest.mark.filterwarnings("ignore:Sparse CSR tensor support is in beta")]
+pytestmark = [pytest.mark.gpu, pytest.mark.filterwarnings("ignore:Sparse CSR tensor support is in beta"),
+              pytest.mark.filterwarnings("ignore:Sparse invariant checks are implicitly disabled")]
 
 torch = pytest.importorskip("torch")
 
