@@ -179,48 +179,13 @@ enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 
 
 // ---- pJDS kernel -----------------------------------------------------------------------------
 
-// Thread t owns the R consecutive sorted rows k0 = R*t .. R*t+R-1 (R divides b_r, so they share
-// one pJDS block and its length).  A warp covers 32R rows = one or several consecutive blocks;
-// lanes of a block loop to that block's length (PAPER.md L219-222 / Listing 2 L233, reading 6).
-// PIPE: software-pipelined main loop (next chunk's val/col loads in flight during the current
-// chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
-// Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
-// WIN: fused remote-gather dist kernel (x = the owners' windows, see gather_x).
-template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false, bool WIN = false>
-__global__ void __launch_bounds__(kThreads)
-pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
-                 const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
-                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
-                 double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off,
-                 const T* const* __restrict__ win, int win_shift) {
-  __shared__ Off s_cs[kSmemCS];
-  __shared__ const T* s_win[WIN ? kMaxWin : 1];
-  if constexpr (WIN)
-    for (int i = threadIdx.x; i < kMaxWin; i += kThreads) s_win[i] = win[i];
-  // execution order of the CTA tiles (storage order, or by original row; results are identical)
-  const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
-  const int64_t t = tile * kThreads + threadIdx.x;
-  constexpr int RS = IL ? 32 : 1;  // distance between a thread's rows
-  const int64_t k0 = IL ? ((t & ~int64_t(31)) * R + (t & 31)) : t * R;
-  const int64_t cta_k0 = tile * kThreads * R;
-  const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
-  // sort window of this CTA (CTAs never straddle windows: sigma is a multiple of the tile size);
-  // its col_start table already includes the window's storage offset (kernel view)
-  col_start += wcs_off[cta_k0 / sigma];
-  const int lim = min(cta_len + 1, kSmemCS);
-  for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
-  __syncthreads();
-  const bool active = k0 < n_pad;
-  if (!active && MODE != STORE_DIRECT_DOT) return;
-  T acc[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = T(0);
-  if (active) {
-  const int64_t warp_k0 = (t & ~int64_t(31)) * R;
-  const int wlen = block_len[warp_k0 / br];
-  const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
-  const uint64_t pol_s = make_policy(pol & 0xff);
-  const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
+// The R row chains of one thread (rows k0 + r*RS, all of length `len`, one jagged column per
+// step): the j-loop of Listing 2 (L231-237) shared by the static and the dynamic-schedule kernel.
+template <typename T, typename Off, int R, int U, bool PIPE, bool IL, bool WIN>
+__device__ __forceinline__ void row_chains(T (&acc)[R], const T* __restrict__ val, const int* __restrict__ col,
+                                           const Off* s_cs, const int64_t* __restrict__ col_start, int64_t k0,
+                                           int len, const T* __restrict__ x, const T* const* s_win, int win_shift,
+                                           uint64_t pol_s, uint64_t pol_x) {
   auto cs = [&](int j) -> Off { return j < kSmemCS ? s_cs[j] : (Off)col_start[j]; };
   int j = 0;
   if (PIPE && U <= len) {
@@ -306,6 +271,51 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = fma_rn(v[u].v[r], xv[u][r], acc[r]);
   }
+}
+
+// Thread t owns the R consecutive sorted rows k0 = R*t .. R*t+R-1 (R divides b_r, so they share
+// one pJDS block and its length).  A warp covers 32R rows = one or several consecutive blocks;
+// lanes of a block loop to that block's length (PAPER.md L219-222 / Listing 2 L233, reading 6).
+// PIPE: software-pipelined main loop (next chunk's val/col loads in flight during the current
+// chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
+// Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
+// WIN: fused remote-gather dist kernel (x = the owners' windows, see gather_x).
+template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false, bool WIN = false>
+__global__ void __launch_bounds__(kThreads)
+pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
+                 const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
+                 T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
+                 double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off,
+                 const T* const* __restrict__ win, int win_shift) {
+  __shared__ Off s_cs[kSmemCS];
+  __shared__ const T* s_win[WIN ? kMaxWin : 1];
+  if constexpr (WIN)
+    for (int i = threadIdx.x; i < kMaxWin; i += kThreads) s_win[i] = win[i];
+  // execution order of the CTA tiles (storage order, or by original row; results are identical)
+  const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
+  const int64_t t = tile * kThreads + threadIdx.x;
+  constexpr int RS = IL ? 32 : 1;  // distance between a thread's rows
+  const int64_t k0 = IL ? ((t & ~int64_t(31)) * R + (t & 31)) : t * R;
+  const int64_t cta_k0 = tile * kThreads * R;
+  const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
+  // sort window of this CTA (CTAs never straddle windows: sigma is a multiple of the tile size);
+  // its col_start table already includes the window's storage offset (kernel view)
+  col_start += wcs_off[cta_k0 / sigma];
+  const int lim = min(cta_len + 1, kSmemCS);
+  for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
+  __syncthreads();
+  const bool active = k0 < n_pad;
+  if (!active && MODE != STORE_DIRECT_DOT) return;
+  T acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = T(0);
+  if (active) {
+  const int64_t warp_k0 = (t & ~int64_t(31)) * R;
+  const int wlen = block_len[warp_k0 / br];
+  const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
+  const uint64_t pol_s = make_policy(pol & 0xff);
+  const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
+  row_chains<T, Off, R, U, PIPE, IL, WIN>(acc, val, col, s_cs, col_start, k0, len, x, s_win, win_shift, pol_s, pol_x);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t k = k0 + r * RS;

@@ -20,13 +20,15 @@ dist.init_process_group("gloo")
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 transport = sys.argv[2] if len(sys.argv) > 2 else "nccl"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-if name == "rand":
+if name in ("rand", "rand_empty"):
     n, rp, col, val = inputs.small("random", 3000, seed=3, max=60)
 else:
     n, rp, col, val = inputs.config_crs(name)
-seg = {"C1": 1024, "C3": 15504, "rand": 1}[name]
+seg = {"C1": 1024, "C3": 15504, "rand": 1, "rand_empty": 1}[name]
 nb = n // seg
 offs = np.array([(nb * r // R) * seg for r in range(R + 1)], np.int64)
+if name == "rand_empty":  # rank 1 owns no rows (it still takes part in every call)
+    offs[1] = offs[2]
 lo, hi = offs[rank], offs[rank + 1]
 x = inputs.vector(n)
 out = {}

@@ -53,7 +53,7 @@ def test_p2p_transport_multiprocess_one_gpu(case, R):
     run_workers(case, R, "p2p", 5, 29740 + R + (10 if case == "rand" else 0))
 
 
-@pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4), ("rand", 8)])
+@pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4), ("rand", 8), ("rand_empty", 3)])
 def test_direct_transport_multiprocess_one_gpu(case, R):
     """PJDS_TRANSPORT_DIRECT (one kernel per call; nonlocal gathers read the owners' IPC-mapped x
     windows; ready/done flags): bitwise equal to the oracle's unsplit FMA chain, both bases, x
@@ -61,7 +61,7 @@ def test_direct_transport_multiprocess_one_gpu(case, R):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA")
-    run_workers(case, R, "direct", 5, 29780 + R + (10 if case == "rand" else 0))
+    run_workers(case, R, "direct", 5, 29780 + R + {"C1": 0, "rand": 10, "rand_empty": 20}[case])
 
 
 @pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4)])
