@@ -415,6 +415,13 @@ int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind);
    local y stores); 2 = auto (default): 1 in the row-only basis or when x exceeds 64 MB, else 0.
    The per-row arithmetic, and therefore y, is identical. */
 int pjds_set_tile_order(int32_t mode);
+/* pjds_set_schedule (process-wide knob; results are identical): 0 = static grid of CTA tiles
+   (default); 1 = dynamic warp tiles (a persistent grid of SMs x resident CTAs whose warps take
+   tiles of 32R sorted rows from a per-handle counter).  Measured slower on every config (the
+   scattered warp tiles lose the L1 reuse of x between adjacent rows); kept as an experiment.  A
+   handle must not run on two streams at once under the dynamic schedule.  Not used by the
+   Lanczos-fused product, sigma-windowed handles or the lane-interleaved variant. */
+int pjds_set_schedule(int32_t mode);
 
 /* Number of kernel launches this library has enqueued (process-wide counter). */
 int64_t pjds_launch_count(void);

@@ -109,6 +109,7 @@ _SIGS = {
     "pjds_set_kernel_variant": [c_i32, c_i32],
     "pjds_set_cache_policy": [c_i32, c_i32],
     "pjds_set_tile_order": [c_i32],
+    "pjds_set_schedule": [c_i32],
     "pjds_set_tile_keys": [c_p, c_p, c_i64],
     "pjds_lanczos": [c_p, c_p, c_i32, c_p, c_p, c_p, c_p],
     "pjds_tridiag_eigenvalues": [c_i32, c_p, c_p, c_p],

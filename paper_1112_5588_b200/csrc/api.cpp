@@ -25,8 +25,9 @@ static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
 
 int free_pjds_device(pjds_mat* A) {
   cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
-  cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off);
+  cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off); cudaFree(A->d_sched);
   A->d_wcs_off = nullptr;
+  A->d_sched = nullptr;
   for (int b = 0; b < 2; ++b) {
     cudaFree(A->d_bx[b]); cudaFree(A->d_by[b]); cudaFree(A->d_bp[b]);
     A->d_bx[b] = A->d_by[b] = A->d_bp[b] = nullptr;
@@ -79,7 +80,8 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
       (s = dmalloc_copy(&A->d_col_start, cs_abs.data(), cs_abs.size() * 8)) ||
       (s = dmalloc_copy(&A->d_wcs_off, woff.data(), woff.size() * 8)) ||
       (s = dmalloc_copy(&A->d_block_len, h.block_len.data(), h.block_len.size() * 4)) ||
-      (s = dmalloc_copy(&A->d_perm, tp, (size_t)h.n * 4))) {
+      (s = dmalloc_copy(&A->d_perm, tp, (size_t)h.n * 4)) ||
+      (s = dmalloc_copy(&A->d_sched, nullptr, 0))) {  // 16 zeroed bytes: the dynamic-schedule counters
     free_pjds_device(A);
     return s;
   }
@@ -416,6 +418,7 @@ int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll) {
 
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind) { return set_cache_policy(stream_kind, x_kind); }
 int pjds_set_tile_order(int32_t mode) { return set_tile_order(mode); }
+int pjds_set_schedule(int32_t mode) { return set_schedule(mode); }
 
 int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n) {
   if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: NULL handle");

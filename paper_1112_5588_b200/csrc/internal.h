@@ -86,6 +86,7 @@ struct pjds_mat {
   // position; d_win = device table of 64 x-window base pointers (owned by the dist handle)
   void** d_win = nullptr;
   int win_shift = 0;
+  unsigned long long* d_sched = nullptr;  // dynamic warp-tile schedule: {next tile, CTAs done}
 };
 
 struct ellr_mat {
@@ -121,6 +122,7 @@ int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int
 int set_kernel_variant(int r, int u);
 int set_cache_policy(int stream_kind, int x_kind);
 int set_tile_order(int mode);
+int set_schedule(int mode);
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
 void count_launch(int64_t k = 1);
 }  // namespace pjds

@@ -348,6 +348,75 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   }
 }
 
+// Dynamic warp-tile schedule (opt-in experiment, pjds_set_schedule(1); measured slower, see g_sched).  A static grid of CTA
+// tiles leaves SMs idle in the last partial wave, and with one wave (DLR1: 544 CTAs) the SMs that
+// drew the longest rows finish last.  Here a persistent grid of (SMs x resident CTAs) warps takes
+// warp tiles of 32R sorted rows from a global counter in storage order -- longest rows first, so
+// the schedule is greedy longest-processing-time -- and runs the same row chains (results are
+// bitwise those of the static kernel).  The last CTA to finish resets the counter, so launches on
+// one stream need no memset (graph-capture safe; a handle must not run on two streams at once).
+template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool WIN>
+__global__ void __launch_bounds__(kThreads)
+pjds_spmv_dyn_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
+                     const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
+                     T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
+                     const T* const* __restrict__ win, int win_shift, int64_t n_slots,
+                     unsigned long long* __restrict__ sched, int width) {
+  __shared__ Off s_cs[kSmemCS];
+  __shared__ const T* s_win[WIN ? kMaxWin : 1];
+  if constexpr (WIN)
+    for (int i = threadIdx.x; i < kMaxWin; i += kThreads) s_win[i] = win[i];
+  const int lim = min(width + 1, kSmemCS);  // the whole table: every warp tile may come here
+  for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol_s = make_policy(pol & 0xff);
+  const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
+  constexpr int kWarpsPerTile = kThreads / 32;
+#pragma unroll 1
+  for (;;) {
+    unsigned long long w = 0;
+    if (lane == 0) w = atomicAdd(&sched[0], 1ull);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    if ((int64_t)w >= n_slots) break;
+    // warp tile -> rows, following the CTA tile order (kWarpsPerTile warp tiles per CTA tile)
+    const int64_t wt = tile_order ? (int64_t)tile_order[w / kWarpsPerTile] * kWarpsPerTile + (int64_t)(w % kWarpsPerTile)
+                                  : (int64_t)w;
+    const int64_t warp_k0 = wt * 32 * R;
+    const int64_t k0 = warp_k0 + (int64_t)lane * R;
+    if (k0 >= n_pad) continue;
+    const int wlen = block_len[warp_k0 / br];
+    const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = T(0);
+    row_chains<T, Off, R, U, PIPE, false, WIN>(acc, val, col, s_cs, col_start, k0, len, x, s_win, win_shift, pol_s,
+                                               pol_x);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t k = k0 + r;
+      if (k < n) {
+        if (MODE == STORE_DIRECT) {
+          y[k] = acc[r];
+        } else {
+          const int p = perm[k];
+          if (MODE == STORE_PERM_ACC) y[p] = y[p] + acc[r];
+          else y[p] = acc[r];
+        }
+      }
+    }
+  }
+  __syncthreads();  // every warp of this CTA is past its last counter read
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&sched[1], 1ull) == (unsigned long long)gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // Long-row ("split-j") variant: S warps share one group of 32 rows so that long
 // rows (DLR1/DLR2/UHBR, N_nzr 123-315) do not leave each thread a long serial chain of dependent
 // gathers.  Warp w of a CTA works on row group w / S as sub s = w % S: lane l owns row
@@ -454,6 +523,73 @@ int set_tile_order_impl(int mode) {
   g_tile_order = mode;
   return PJDS_OK;
 }
+// 0 static CTA grid (default), 1 dynamic warp tiles.  Measured (profiles/r01_kbench_schedule.jsonl):
+// dynamic is slower on every config -- C4 DP 80 -> 146 us, W4 DP 310 -> 540, C2 DP 58 -> 60,
+// C5 DP 2045 -> 2184 -- because warp tiles handed out in arrival order scatter adjacent row tiles
+// over different SMs, and the block-structured matrices (DLR1/DLR2: 6 or 5 consecutive rows share
+// their x entries) lose the L1 reuse that a CTA of 8 adjacent warp tiles gets on one SM.
+static int g_sched = 0;
+
+int set_schedule_impl(int mode) {
+  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "schedule: 0 static, 1 dynamic warp tiles");
+  g_sched = mode;
+  return PJDS_OK;
+}
+
+static int num_sms() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) v = 148;
+  }
+  return v;
+}
+
+// Launch the dynamic warp-tile kernel when the schedule asks for it.  *launched = false leaves the
+// static launch to the caller.
+template <typename T, typename Off, int R, int U, int M, bool PF, bool W>
+int launch_dyn(const pjds_mat* A, T* y, const T* x, cudaStream_t s, const int* order, int64_t grid_static,
+               bool* launched) {
+  *launched = false;
+  if (g_sched == 0) return PJDS_OK;
+  static int occ = 0;
+  auto kern = pjds_spmv_dyn_kernel<T, Off, R, U, M, PF, W>;
+  if (!occ) {
+    PJDS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+    occ = std::max(occ, 1);
+  }
+  const int64_t cap = (int64_t)num_sms() * occ;
+  (void)grid_static;
+  const auto& h = A->h;
+  // warp-tile slots: every CTA tile of the order contributes kThreads/32 slots (the partial last
+  // CTA tile can sit anywhere in the order; its slots past the matrix are skipped in the kernel)
+  const int64_t wpt = kThreads / 32;
+  const int64_t n_wtiles = (h.n_pad + 32 * R - 1) / (32 * R);
+  const int64_t n_slots = (n_wtiles + wpt - 1) / wpt * wpt;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(cap, n_slots / wpt));
+  kern<<<(unsigned)grid, kThreads, 0, s>>>((const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x,
+                                           y, h.n, h.n_pad, h.br, g_pol, order, (const T* const*)A->d_win,
+                                           A->win_shift, n_slots, A->d_sched, h.width);
+  count_launch();
+  PJDS_CUDA_TRY(cudaGetLastError());
+  *launched = true;
+  return PJDS_OK;
+}
+
+template <typename T, typename Off, int R, int U, int M>
+int launch_dyn_any(const pjds_mat* A, T* y, const T* x, cudaStream_t s, const int* order, int64_t grid_static,
+                   bool pipe, bool* launched) {
+  *launched = false;
+  if (A->d_win) {  // window matrices: y = A x only, 32-bit offsets (else the static path reports it)
+    if constexpr (std::is_same<Off, int32_t>::value && M != STORE_PERM_ACC)
+      return launch_dyn<T, Off, R, U, M, false, true>(A, y, x, s, order, grid_static, launched);
+    return PJDS_OK;
+  }
+  if (pipe) return launch_dyn<T, Off, R, U, M, true, false>(A, y, x, s, order, grid_static, launched);
+  return launch_dyn<T, Off, R, U, M, false, false>(A, y, x, s, order, grid_static, launched);
+}
+
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
 static bool g_il = false;    // lane-interleaved rows (variant knob unroll + 32; needs b_r % (32 R) == 0)
 
@@ -473,6 +609,16 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
                       (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
                        (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(A, R, &order));
+  // grids of a few waves: dynamic warp tiles (same row chains, bitwise the same y)
+  if (A->d_sched && h.n_windows <= 1 && !(g_il && R > 1) && mode != STORE_DIRECT_DOT) {
+    bool done = false;
+int st;
+    if (mode == STORE_DIRECT) st = launch_dyn_any<T, Off, R, U, STORE_DIRECT>(A, y, x, s, order, grid, pipe, &done);
+    else if (mode == STORE_PERM_ACC) st = launch_dyn_any<T, Off, R, U, STORE_PERM_ACC>(A, y, x, s, order, grid, pipe, &done);
+    else st = launch_dyn_any<T, Off, R, U, STORE_PERM>(A, y, x, s, order, grid, pipe, &done);
+    if (st != PJDS_OK) return st;
+    if (done) return PJDS_OK;
+  }
 #define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
   pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part, h.sigma, \
@@ -703,6 +849,7 @@ int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t
 }
 
 int set_tile_order(int mode) { return set_tile_order_impl(mode); }
+int set_schedule(int mode) { return set_schedule_impl(mode); }
 
 int set_cache_policy(int stream_kind, int x_kind) {
   if (stream_kind < 0 || stream_kind > 3 || x_kind < 0 || x_kind > 3)

@@ -424,3 +424,40 @@ def test_spmv_host_batch_pipelined(pj, symmetric):
     A.spmv_host_batch(ys, xs)
     for x, y in zip(xs, ys):
         check_y(y, n, rp, col, val, x)
+
+
+@pytest.mark.parametrize("sched", [0, 1])
+def test_schedule_bitwise(pj, sched):
+    """pjds_set_schedule: the dynamic warp-tile kernel runs the same row chains as the static grid
+    (bitwise = the FMA chain), for every rows-per-thread variant, the pipelined variant, both
+    bases, both tile orders, ragged warp tiles, and repeated launches (its counter resets itself)."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_schedule(sched) == 0
+        cases = [("C4", None), ("C1", None), ("random", 1500), ("adversarial", 1000), ("empty_rows", 513)]
+        for name, m in cases:
+            for dtype in (np.float64, np.float32):
+                if m is None:
+                    n, rp, col, val = inputs.config_crs(name, dtype=dtype)
+                else:
+                    n, rp, col, val = inputs.small(name, m, seed=m, dtype=dtype, **({"max": 90} if name == "random" else {}))
+                x = inputs.vector(n, dtype)
+                xt = tdev(x)
+                for sym in (False, True):
+                    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=sym)
+                    xin = A.to_permuted(torch.empty_like(xt), xt) if sym else xt
+                    for variant in ((0, 0), (1, 8), (2, 4), (4, 2), (2, 20)):
+                        assert L.pjds_set_kernel_variant(*variant) == 0
+                        for order in (0, 1):
+                            assert L.pjds_set_tile_order(order) == 0
+                            y = torch.full_like(xt, float("nan"))
+                            for _ in range(3):
+                                A.spmv(y, xin)
+                            yo = A.from_permuted(torch.empty_like(y), y) if sym else y
+                            torch.cuda.synchronize()
+                            check_y(yo.cpu().numpy(), n, rp, col, val, x)
+                    del A
+    finally:
+        L.pjds_set_schedule(0)
+        L.pjds_set_kernel_variant(0, 0)
+        L.pjds_set_tile_order(2)

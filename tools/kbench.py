@@ -29,6 +29,7 @@ p.add_argument("--reps", type=int, default=30)
 p.add_argument("--variants", default="0x0")
 p.add_argument("--policies", default="1x2")
 p.add_argument("--orders", default="2")
+p.add_argument("--scheds", default="0", help="0 static CTA grid, 1 dynamic warp tiles")
 p.add_argument("--sigmas", default="0")
 p.add_argument("--keys", default="none", help="tile keys: none (original index) or wW = HMEp phonon window of W rows")
 SEG = {"C1": 1024, "C3": 15504, "C5": 142506}
@@ -53,8 +54,10 @@ for cfg in a.configs.split(","):
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
           pj.bw_probe(1 << 30, 20)  # host-side conversion leaves the GPU idle: re-raise clocks
-          for var, polk, order, kspec in [(v, q, o, kk) for v in a.variants.split(",") for q in a.policies.split(",")
-                                          for o in a.orders.split(",") for kk in a.keys.split(",")]:
+          for var, polk, order, kspec, sch in [(v, q, o, kk, sc) for v in a.variants.split(",") for q in a.policies.split(",")
+                                               for o in a.orders.split(",") for kk in a.keys.split(",")
+                                               for sc in a.scheds.split(",")]:
+            pj.lib().pjds_set_schedule(int(sch))
             if fmt.startswith("pjds"):
                 if kspec == "none":
                     A.set_tile_keys(None)
@@ -78,7 +81,7 @@ for cfg in a.configs.split(","):
             ck = clocks()
             e1.record(); torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
-            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "keys": kspec, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sched": int(sch), "keys": kspec, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
                               "stored_bytes": A.info.get("bytes_total"), "clk": ck}), flush=True)
           del A
