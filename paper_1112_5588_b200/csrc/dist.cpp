@@ -168,6 +168,7 @@ struct pjds_dist {
   int32_t win_shift = 0;
   void** d_win = nullptr;                       // [kWinTable] x-window base per owner rank
   std::vector<int32_t> dir_send_pos;            // my window position of every send entry (send order)
+  bool dir_cols_encoded = false;                // column codes rewritten (connect is not retryable after)
   std::vector<int64_t> offsets;                 // row offsets [R+1]
   uint64_t* ready_flags() const { return (uint64_t*)(p2p_region + p2p_flags_off); }
   uint64_t* done_flags() const { return ready_flags() + R; }
@@ -695,6 +696,8 @@ int pjds_dist_direct_connect(pjds_dist_t D, const int32_t* halo_pos, const void*
   if (!D || !blobs) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: NULL argument");
   if (D->transport != PJDS_TRANSPORT_DIRECT) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: not a DIRECT handle");
   if (D->p2p_connected) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: already connected");
+  if (D->dir_cols_encoded) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: an earlier connect failed after "
+                                                                 "rewriting the columns; destroy the handle");
   if (D->halo > 0 && !halo_pos) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: NULL halo_pos");
   if (blob_bytes != (int64_t)sizeof(P2PBlob)) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_direct_connect: blob size");
   const P2PBlob* b = (const P2PBlob*)blobs;
@@ -740,6 +743,7 @@ int pjds_dist_direct_connect(pjds_dist_t D, const int32_t* halo_pos, const void*
   std::vector<int32_t> inv(nl);
   for (int64_t k = 0; k < nl; ++k) inv[h.perm[k]] = D->permuted ? (int32_t)k : h.perm[k];
   const int32_t me = D->rank << sh;
+  D->dir_cols_encoded = true;
 #pragma omp parallel for
   for (int64_t k = 0; k < (int64_t)h.col.size(); ++k) {
     const int32_t c = h.col[k];
