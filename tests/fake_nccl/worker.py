@@ -20,17 +20,18 @@ dist.init_process_group("gloo")
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 transport = sys.argv[2] if len(sys.argv) > 2 else "nccl"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+npdt = np.float32 if (len(sys.argv) > 4 and sys.argv[4] == "f32") else np.float64
 if name in ("rand", "rand_empty"):
-    n, rp, col, val = inputs.small("random", 3000, seed=3, max=60)
+    n, rp, col, val = inputs.small("random", 3000, seed=3, max=60, dtype=npdt)
 else:
-    n, rp, col, val = inputs.config_crs(name)
+    n, rp, col, val = inputs.config_crs(name, dtype=npdt)
 seg = {"C1": 1024, "C3": 15504, "rand": 1, "rand_empty": 1}[name]
 nb = n // seg
 offs = np.array([(nb * r // R) * seg for r in range(R + 1)], np.int64)
 if name == "rand_empty":  # rank 1 owns no rows (it still takes part in every call)
     offs[1] = offs[2]
 lo, hi = offs[rank], offs[rank + 1]
-x = inputs.vector(n)
+x = inputs.vector(n, npdt)
 out = {}
 # DIRECT: one kernel over the unsplit rows -> bitwise the plain FMA chain; others: the split rule
 chain = oracle.spmv_chain(n, rp, col, val, x) if transport == "direct" else None
@@ -59,7 +60,7 @@ for permuted in (False, True):
         yall = np.concatenate(ys)
         ref = chain if chain is not None else (odist.spmv(odist.split(n, rp, col, val, offs), x) if name != "C3" else None)
         yl, b = oracle.spmv_ld(n, rp, col, val, x)
-        ok = bool(oracle.acceptance(yall, yl, b, np.diff(rp), np.float64).all())
+        ok = bool(oracle.acceptance(yall, yl, b, np.diff(rp), npdt).all())
         out[f"perm{int(permuted)}_noov{int(no)}"] = {"o2": ok, "bitwise_vs_split_oracle": bool(np.array_equal(yall, ref)) if ref is not None else None,
                                                      "trace": D.trace(), "halo": D.info["halo"], "messages": D.info["send_messages"],
                                                      "timed_out": D.p2p_timed_out()}

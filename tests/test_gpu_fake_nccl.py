@@ -25,13 +25,13 @@ def build_fake():
     return out
 
 
-def run_workers(case, R, transport, reps, port):
+def run_workers(case, R, transport, reps, port, dtype="f64"):
     env = dict(os.environ, OMP_NUM_THREADS="1")
     if transport == "nccl":
         env["PJDS_NCCL_LIB"] = build_fake()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={R}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.join(HERE, "worker.py"), case, transport,
-           str(reps)]
+           str(reps), dtype]
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     assert p.returncode == 0 and len(lines) == R, p.stdout[-2000:] + p.stderr[-3000:]
@@ -53,15 +53,17 @@ def test_p2p_transport_multiprocess_one_gpu(case, R):
     run_workers(case, R, "p2p", 5, 29740 + R + (10 if case == "rand" else 0))
 
 
-@pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4), ("rand", 8), ("rand_empty", 3)])
-def test_direct_transport_multiprocess_one_gpu(case, R):
+@pytest.mark.parametrize("case,R,dtype", [("C1", 2, "f64"), ("rand", 3, "f64"), ("C1", 4, "f64"), ("rand", 8, "f64"),
+                                          ("rand_empty", 3, "f64"), ("C1", 2, "f32"), ("rand", 4, "f32")])
+def test_direct_transport_multiprocess_one_gpu(case, R, dtype):
     """PJDS_TRANSPORT_DIRECT (one kernel per call; nonlocal gathers read the owners' IPC-mapped x
     windows; ready/done flags): bitwise equal to the oracle's unsplit FMA chain, both bases, x
     passed separately (copied into the window) and computed in the window, several calls."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA")
-    run_workers(case, R, "direct", 5, 29780 + R + {"C1": 0, "rand": 10, "rand_empty": 20}[case])
+    run_workers(case, R, "direct", 5, 29780 + R + {"C1": 0, "rand": 10, "rand_empty": 20}[case] + (30 if dtype == "f32" else 0),
+                dtype)
 
 
 @pytest.mark.parametrize("case,R", [("C1", 2), ("rand", 3), ("C1", 4)])
