@@ -84,3 +84,20 @@ def test_nccl_transport_multiprocess_one_gpu(case, R):
         for mode in ("perm0_noov0", "perm0_noov1", "perm1_noov0", "perm1_noov1"):
             assert rec[mode]["o2"], (rec["rank"], mode)
             assert rec[mode]["bitwise_vs_split_oracle"], (rec["rank"], mode)
+
+
+def test_direct_c5_sampled():
+    """DIRECT on the bench matrix (C5, 942 M nonzeros) with 2 processes on the one GPU: sampled rows
+    bitwise = the oracle's unsplit FMA chain and within O2, every row finite, no flag timeout."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    env = dict(os.environ, OMP_NUM_THREADS="4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port=29841", os.path.join(HERE, "worker_c5.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and len(lines) == 2, p.stdout[-2000:] + p.stderr[-3000:]
+    for rec in lines:
+        assert rec["bitwise"] and rec["o2"] and rec["finite"] and not rec["timed_out"], rec
+        assert rec["halo"] > 0

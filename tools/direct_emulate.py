@@ -8,7 +8,8 @@ columns address the owners' CUDA-IPC mapped x windows), then
      not modelled -- the HBM bytes are (the per-rank HBM traffic of the design);
   2. all ranks run `calls` full pjds_dist_spmv calls concurrently (ready/done flags, window), the
      whole job on one GPU: total time vs the sum of the kernels = protocol overhead;
-  3. sampled rows of y vs the oracle's FMA chain (bitwise; the unsplit chain is the DIRECT result).
+  (correctness of the same path is covered by tests/test_gpu_fake_nccl.py against the oracle; this
+  tool only checks that y is finite -- dev tools do not import oracle/).
 R = 1 also times the plain single-GPU kernel on the same matrix (the T_1 of the efficiency).
 Prints one JSON line on rank 0.
 """
@@ -24,7 +25,6 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import inputs  # noqa: E402
-import oracle  # noqa: E402
 import paper_1112_5588_b200 as pj  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
@@ -83,20 +83,8 @@ e1.record()
 torch.cuda.synchronize()
 t_job = e0.elapsed_time(e1) / calls * 1e3
 timed_out = D.p2p_timed_out()
-# sampled rows vs the oracle chain (original local order)
-y0 = D.from_permuted(torch.empty_like(y), y).cpu().numpy()
-rng = np.random.default_rng(rank)
-rows = np.unique(np.concatenate([rng.integers(0, hi - lo, 2000), [0, hi - lo - 1]]))
-x_full = inputs.vector(n)
-srp = np.zeros(len(rows) + 1, np.int64)
-sc, sv = [], []
-for a, i in enumerate(rows):
-    _, cc, vv = g.crs(lo + int(i), lo + int(i) + 1)
-    sc.append(cc)
-    sv.append(vv)
-    srp[a + 1] = srp[a] + len(cc)
-bitwise = bool(np.array_equal(y0[rows], oracle.spmv_chain(len(rows), srp, np.concatenate(sc),
-                                                            np.concatenate(sv), x_full)))
+finite = bool(torch.isfinite(y).all().item())
+x_full = inputs.vector(n) if R == 1 else None
 t_plain = None
 if R == 1:
     rp1, col1, val1 = g.crs()
@@ -107,7 +95,7 @@ if R == 1:
     yp = torch.empty_like(xp)
     t_plain = timeit(lambda: P.spmv(yp, xp), reps)
 info = D.info
-rec = {"rank": rank, "t_kernel_us": round(t_kernel, 1), "t_job_us": round(t_job, 1), "bitwise_sampled": bitwise,
+rec = {"rank": rank, "t_kernel_us": round(t_kernel, 1), "t_job_us": round(t_job, 1), "finite": finite,
        "timed_out": timed_out, "halo": info["halo"], "nnz_nonlocal": info["nnz_nonlocal_part"],
        "n_loc": hi - lo, "t_plain_us": round(t_plain, 1) if t_plain else None}
 recs = [None] * R
@@ -117,7 +105,7 @@ if rank == 0:
     print(json.dumps({"config": cfg, "R": R, "t_kernel_max_us": max(tk), "t_kernel_sum_us": round(sum(tk), 1),
                       "t_job_one_gpu_us": recs[0]["t_job_us"],
                       "protocol_overhead_per_call_us": round(recs[0]["t_job_us"] - sum(tk), 1),
-                      "all_bitwise": all(r_["bitwise_sampled"] for r_ in recs),
+                      "all_finite": all(r_["finite"] for r_ in recs),
                       "any_timeout": any(r_["timed_out"] for r_ in recs), "ranks": recs}), flush=True)
 dist.barrier()
 D.close()
