@@ -73,8 +73,12 @@ for cfg in a.configs.split(","):
 
             if a.once:
                 A.spmv(y, x); torch.cuda.synchronize(); continue
-            for _ in range(5): A.spmv(y, x)
-            torch.cuda.synchronize()
+            # warm-up by time, not by count: after the host-side matrix build the GPU has idled and
+            # its clocks ramp for tens of ms (a 5-launch warm-up left the first variant 25 % slow)
+            t_w = time.perf_counter()
+            while time.perf_counter() - t_w < 0.1:
+                for _ in range(5): A.spmv(y, x)
+                torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(a.reps): A.spmv(y, x)
