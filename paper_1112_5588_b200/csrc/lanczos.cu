@@ -10,10 +10,10 @@
 // scaling pass is needed:
 //   K1  y = A u_j, with per-CTA partial sums of y . u_j fused into the pJDS kernel's epilogue
 //       (STORE_DIRECT_DOT: in the permuted basis u_j[k] is the input entry of row k)
-//   R1  alpha_j = c_j^2 * sum                      (one CTA, fixed-order tree: deterministic)
+//   R1  alpha_j = c_j^2 * sum                      (148 CTAs + last-CTA sum, fixed order: deterministic)
 //   K3  u_{j+1} = c_j y - alpha_j c_j u_j - beta_{j-1} c_{j-1} u_{j-1}  (in place of u_{j-1}),
 //       partial sums of u_{j+1} . u_{j+1}
-//   R2  beta_j = sqrt(sum), c_{j+1} = 1 / beta_j
+//   R2  beta_j = sqrt(sum), c_{j+1} = 1 / beta_j  (fused into K3: its last CTA to finish)
 // All m iterations are captured once into a CUDA graph and launched on the caller's stream.
 // Dot products accumulate in double for both SP and DP vectors.
 #include <algorithm>
@@ -26,6 +26,7 @@ namespace {
 
 constexpr int kRedThreads = 256;
 constexpr int kRedCTAs = 148 * 8;  // vector passes: 8 CTAs per SM, 4 elements in flight per thread
+constexpr int kAlphaCTAs = 148;    // R1: one CTA per SM, then one CTA sums their 148 results
 
 __device__ __forceinline__ double block_sum(double v, double* sm) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -50,34 +51,60 @@ __global__ void __launch_bounds__(kRedThreads) dot_partials(const T* __restrict_
 }
 
 // scal layout: c[j] at scal[j] (j = 0..m), alpha[j] at scal[(m+1) + j], beta[j] at scal[(m+1)+m + j]
-__global__ void reduce_alpha(const double* __restrict__ part, int np, double* scal, int m, int j) {
-  __shared__ double sm[32];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
-  s = block_sum(s, sm);
-  if (threadIdx.x == 0) {
-    const double c = scal[j];
-    scal[(m + 1) + j] = s * c * c;
+// One CTA sums the np partials in a fixed order (deterministic).  Eight independent loads per
+// thread per round: a plain strided loop waits one L2 round trip per element (C5: 55.7 K
+// partials of the product's CTAs took 28 us; measured with tools/lanczos_bench.py)
+// CG: L2-coherent loads (__ldcg) for partials written by other CTAs of the running grid.
+template <bool CG = false>
+__device__ __forceinline__ double sum_partials(const double* part, int np, double* sm) {
+  constexpr int kIn = 8;
+  double s[kIn];
+#pragma unroll
+  for (int q = 0; q < kIn; ++q) s[q] = 0.0;
+  const int bd = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + (kIn - 1) * bd < np; i += kIn * bd) {
+    double v[kIn];
+#pragma unroll
+    for (int q = 0; q < kIn; ++q) v[q] = CG ? __ldcg(part + i + q * bd) : part[i + q * bd];
+#pragma unroll
+    for (int q = 0; q < kIn; ++q) s[q] += v[q];
   }
+  for (; i < np; i += bd) s[0] += CG ? __ldcg(part + i) : part[i];  // < kIn ragged rounds
+  const double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  return block_sum(t, sm);  // valid in thread 0
 }
 
-__global__ void reduce_beta(const double* __restrict__ part, int np, double* scal, int m, int j) {
+// R1 over many CTAs: CTA b sums its contiguous chunk of the product's partials, the last CTA to
+// finish sums the per-CTA results (fixed order: deterministic) and writes alpha_j
+__global__ void __launch_bounds__(kRedThreads) reduce_alpha(const double* __restrict__ part, int np, double* part2,
+                                                             unsigned* ctr, double* scal, int m, int j) {
   __shared__ double sm[32];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
-  s = block_sum(s, sm);
+  __shared__ bool last;
+  const int chunk = (np + gridDim.x - 1) / gridDim.x;
+  const int lo = min(np, (int)blockIdx.x * chunk), hi = min(np, lo + chunk);
+  const double s = sum_partials(part + lo, hi - lo, sm);
   if (threadIdx.x == 0) {
-    const double b = sqrt(s);
-    scal[(m + 1) + m + j] = b;
-    scal[j + 1] = b > 0.0 ? 1.0 / b : 0.0;
+    part2[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double t = sum_partials<true>(part2, gridDim.x, sm);
+  if (threadIdx.x == 0) {
+    const double c = scal[j];
+    scal[(m + 1) + j] = t * c * c;
+    *ctr = 0u;
   }
 }
 
 // u_next (aliases u_prev) = c_j y - alpha_j c_j u_j - beta_{j-1} c_{j-1} u_prev ; partial |u_next|^2
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) lanczos_update(const T* __restrict__ y, const T* __restrict__ u,
-                                                              T* u_prev_next, int64_t n, const double* __restrict__ scal,
-                                                              int m, int j, double* __restrict__ part) {
+                                                              T* u_prev_next, int64_t n, double* scal,
+                                                              int m, int j, double* part, unsigned* ctr) {
   __shared__ double sm[32];
   const double cj = scal[j];
   const double aj = scal[(m + 1) + j];
@@ -109,14 +136,28 @@ __global__ void __launch_bounds__(kRedThreads) lanczos_update(const T* __restric
     s = fma((double)vt, (double)vt, s);
   }
   s = block_sum(s, sm);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  // R2 fused: the last CTA to finish sums the partials (fixed order) and writes beta_j, c_{j+1}
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double t = sum_partials<true>(part, gridDim.x, sm);
+  if (threadIdx.x == 0) {
+    const double b = sqrt(t);
+    scal[(m + 1) + m + j] = b;
+    scal[j + 1] = b > 0.0 ? 1.0 / b : 0.0;
+    *ctr = 0u;  // ready for the next step's launch
+  }
 }
 
 __global__ void init_c0(const double* __restrict__ part, int np, double* scal) {
   __shared__ double sm[32];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
-  s = block_sum(s, sm);
+  const double s = sum_partials(part, np, sm);
   if (threadIdx.x == 0) scal[0] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
 }
 
@@ -126,6 +167,7 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
   const size_t vb = (size_t)n * sizeof(T);
   T *u0 = nullptr, *u1 = nullptr, *y = nullptr;
   double *part = nullptr, *scal = nullptr;
+  unsigned* ctr = nullptr;
   cudaStream_t s = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -134,7 +176,7 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (s) cudaStreamDestroy(s);
-    cudaFree(u0); cudaFree(u1); cudaFree(y); cudaFree(part); cudaFree(scal);
+    cudaFree(u0); cudaFree(u1); cudaFree(y); cudaFree(part); cudaFree(scal); cudaFree(ctr);
   };
 #define LZ_TRY(expr)                                                                   \
   do {                                                                                 \
@@ -150,8 +192,10 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
   LZ_TRY(cudaMalloc(&u1, vb ? vb : 16));
   LZ_TRY(cudaMalloc(&y, vb ? vb : 16));
   const int64_t np_max = std::max<int64_t>(kRedCTAs, A->h.n_pad / 32 + 1);  // <= 8 threads per row
-  LZ_TRY(cudaMalloc(&part, np_max * sizeof(double)));
+  LZ_TRY(cudaMalloc(&part, (np_max + kAlphaCTAs) * sizeof(double)));  // + R1's second level
   LZ_TRY(cudaMalloc(&scal, (size_t)(3 * m + 1) * sizeof(double)));
+  LZ_TRY(cudaMalloc(&ctr, 2 * sizeof(unsigned)));  // [0] update (R2), [1] reduce_alpha (R1)
+  LZ_TRY(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned), user));
   LZ_TRY(cudaMemsetAsync(scal, 0, (size_t)(3 * m + 1) * sizeof(double), user));
   LZ_TRY(cudaMemcpyAsync(u0, v0, vb, cudaMemcpyDeviceToDevice, user));
   // prepare lazily-built kernel state (tile order) outside the capture
@@ -170,12 +214,11 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
       cleanup();
       return st;
     }
-    reduce_alpha<<<1, 1024, 0, s>>>(part, (int)np, scal, m, j);
-    lanczos_update<T><<<kRedCTAs, kRedThreads, 0, s>>>(y, uj, up, n, scal, m, j, part);
-    reduce_beta<<<1, 1024, 0, s>>>(part, kRedCTAs, scal, m, j);
+    reduce_alpha<<<kAlphaCTAs, kRedThreads, 0, s>>>(part, (int)np, part + np_max, ctr + 1, scal, m, j);
+    lanczos_update<T><<<kRedCTAs, kRedThreads, 0, s>>>(y, uj, up, n, scal, m, j, part, ctr);
     std::swap(uj, up);
   }
-  count_launch(2 + 3 * (int64_t)m);
+  count_launch(2 + 3 * (int64_t)m - m);
   LZ_TRY(cudaStreamEndCapture(s, &graph));
   LZ_TRY(cudaGraphInstantiate(&exec, graph, 0));
   LZ_TRY(cudaGraphLaunch(exec, user));

@@ -28,6 +28,21 @@ for _ in range(m): A.spmv(y, v0)
 e1.record(); torch.cuda.synchronize()
 ts = e0.elapsed_time(e1) * 1e-3
 ev = pj.tridiag_eigenvalues(a[:steps], b[:steps])
+# device span of the Lanczos graph (first kernel start to last kernel end, CUPTI via torch.profiler):
+# the wall time above also counts the host setup (vector allocation, graph capture + instantiate)
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    A.lanczos(v0, m)
+    torch.cuda.synchronize()
+kern = [e for e in prof.events() if e.device_type.name == "CUDA" and
+        any(k in e.name for k in ("pjds_spmv", "lanczos_update", "reduce_alpha", "reduce_beta", "dot_partials", "init_c0"))]
+span = (max(e.time_range.end for e in kern) - min(e.time_range.start for e in kern)) * 1e-6 if kern else float("nan")
+busy = {}
+for e in kern:
+    key = next(k for k in ("pjds_spmv", "lanczos_update", "reduce_alpha", "reduce_beta", "dot_partials", "init_c0") if k in e.name)
+    busy[key] = busy.get(key, 0.0) + (e.time_range.end - e.time_range.start) * 1e-6
+print(json.dumps({"device_span_per_step_ms": round(span / m * 1e3, 4), "device_overhead_frac": round(span / ts - 1, 3),
+                  "kernel_ms_per_step": {k: round(v / m * 1e3, 4) for k, v in busy.items()}, "n_kernels": len(kern)}))
 print(json.dumps({"config": cfg, "m": m, "steps": steps, "lanczos_s": round(t, 4), "per_step_ms": round(t / m * 1e3, 3),
                   "spmv_only_per_step_ms": round(ts / m * 1e3, 3), "overhead_frac": round(t / ts - 1, 3),
                   "spmv_gflops_in_lanczos": round(2 * nnz * m / t / 1e9, 1), "ritz_min": ev[0], "ritz_max": ev[-1]}))
