@@ -331,20 +331,14 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   }
   }  // active
   if (MODE == STORE_DIRECT_DOT) {
-    __shared__ double s_red[kThreads / 32];
+    // one partial per warp (no CTA barrier: a warp's lanes leave as soon as their warp is done)
     double d = 0.0;
     if (active)
 #pragma unroll
       for (int r = 0; r < R; ++r)
         if (k0 + r * RS < n) d = fma((double)acc[r], (double)x[k0 + r * RS], d);
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tsum = 0.0;
-      for (int w = 0; w < kThreads / 32; ++w) tsum += s_red[w];
-      dot_part[blockIdx.x] = tsum;
-    }
+    if ((threadIdx.x & 31) == 0) dot_part[blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)] = d;
   }
 }
 
@@ -599,7 +593,7 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   const auto& h = A->h;
   const int64_t threads = h.n_pad / R;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
-  if (nparts) *nparts = grid;
+  if (nparts) *nparts = grid * (kThreads / 32);  // STORE_DIRECT_DOT: one partial per warp
   if (grid == 0) return PJDS_OK;
   const int* order = nullptr;
   // auto: original-row order when y is scattered through perm (keeps the stores of a region

@@ -191,7 +191,8 @@ int lanczos_t(pjds_mat* A, const void* v0, int m, double* alpha, double* beta, i
   LZ_TRY(cudaMalloc(&u0, vb ? vb : 16));
   LZ_TRY(cudaMalloc(&u1, vb ? vb : 16));
   LZ_TRY(cudaMalloc(&y, vb ? vb : 16));
-  const int64_t np_max = std::max<int64_t>(kRedCTAs, A->h.n_pad / 32 + 1);  // <= 8 threads per row
+  // product partials: one per warp (<= n_pad / 32 + 8) or one per CTA of the split kernel (<= n_pad / 32)
+  const int64_t np_max = std::max<int64_t>(kRedCTAs, A->h.n_pad / 32 + 64);
   LZ_TRY(cudaMalloc(&part, (np_max + kAlphaCTAs) * sizeof(double)));  // + R1's second level
   LZ_TRY(cudaMalloc(&scal, (size_t)(3 * m + 1) * sizeof(double)));
   LZ_TRY(cudaMalloc(&ctr, 2 * sizeof(unsigned)));  // [0] update (R2), [1] reduce_alpha (R1)
