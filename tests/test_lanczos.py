@@ -98,6 +98,28 @@ def test_gpu_lanczos_matches_oracle(dtype):
 
 
 @pytest.mark.gpu
+def test_gpu_lanczos_many_product_partials():
+    """n_pad = 40,032 runs the one-row-per-thread kernel: 157 CTAs x 8 warps = 1,256 per-warp dot
+    partials, more than the update pass's 1,184 and than n_pad / 32 + 1 (the partial buffer and the
+    two-level alpha reduce must hold them all)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    import paper_1112_5588_b200 as pj
+    n, rp, col, val = sym_matrix(40001, 11)
+    v0 = inputs.vector(n, np.float64, seed=78)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+    perm = A.export()["perm"]
+    m = 12
+    a, b, steps = A.lanczos(torch.from_numpy(v0[perm].copy()).cuda(), m)
+    assert steps == m
+    ra, rb = olz.lanczos(n, rp, col, val, v0, m)
+    scale = max(np.abs(ra).max(), np.abs(rb).max())
+    assert np.abs(a - ra).max() <= 1e-10 * scale
+    assert np.abs(b - rb).max() <= 1e-10 * scale
+
+
+@pytest.mark.gpu
 def test_gpu_lanczos_breakdown_and_zero_start():
     """A = 2 I with v0 = e_0: alpha_0 = 2 and w = 0 exactly, so the recurrence stops after one step
     (steps_done = 1), as the oracle does; a zero start vector is rejected."""
