@@ -363,8 +363,9 @@ int pjds_nccl_unique_id(void* out128);
  * Precondition: A symmetric (not checked).  v0: device vector (permuted basis, handle dtype, n
  * entries, not modified; INVALID_ARG if its norm is 0).  alpha[m], beta[m]: host outputs (double).
  * *steps_done = m, or j+1 if beta_j = 0 exactly (invariant subspace; entries past steps_done are
- * unspecified).  Dot products accumulate in double.  The m iterations (pJDS
- * kernel + 2 fused vector passes + 2 one-CTA reductions each) are captured into one CUDA graph and
+ * unspecified).  Dot products accumulate in double.  The m iterations (pJDS kernel with the
+ * alpha partials fused into its epilogue, a two-level deterministic alpha reduce, and the vector
+ * update whose last CTA computes beta: 3 launches each) are captured into one CUDA graph and
  * launched on `stream`; the call synchronises `stream`.  Work buffers (3 vectors) are allocated
  * and freed inside.
  */
