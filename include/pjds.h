@@ -407,7 +407,10 @@ int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n);
 
 /* Tuning knob (process-wide): L2 eviction priority of the pJDS kernel's streamed val/col loads
    and of its x gathers; kinds 0 evict_normal, 1 evict_first, 2 evict_last, 3 evict_unchanged.
-   Default (1, 2).  Results are unaffected. */
+   Bits 8-15 of stream_kind select the y store of the permuted-basis kernel: 0 = plain scalar
+   stores, 1 + kind = one R-wide vector store per thread with that L2 kind.  Default: stream 1,
+   x 2, y 2 (vector, evict_first; the Lanczos product keeps evict_normal for its y).  Results are
+   unaffected. */
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind);
 
 /* Tuning knob (process-wide): execution order of the pJDS kernel's CTA tiles.  0 = storage

@@ -153,6 +153,26 @@ template <> struct Vec<int, 4> {
   }
 };
 
+// R-wide vector store of a thread's R consecutive results with an L2 policy (y-store experiment)
+template <typename T, int R>
+__device__ __forceinline__ void st_rows(T* p, const T (&a)[R], uint64_t pol) {
+  if constexpr (sizeof(T) == 8 && R == 4)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p), "d"((double)a[0]), "d"((double)a[1]), "d"((double)a[2]), "d"((double)a[3]), "l"(pol) : "memory");
+  else if constexpr (sizeof(T) == 8 && R == 2)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;"
+                 :: "l"(p), "d"((double)a[0]), "d"((double)a[1]), "l"(pol) : "memory");
+  else if constexpr (sizeof(T) == 4 && R == 4)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p), "f"((float)a[0]), "f"((float)a[1]), "f"((float)a[2]), "f"((float)a[3]), "l"(pol) : "memory");
+  else if constexpr (sizeof(T) == 4 && R == 2)
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;"
+                 :: "l"(p), "f"((float)a[0]), "f"((float)a[1]), "l"(pol) : "memory");
+  else
+#pragma unroll
+    for (int r = 0; r < R; ++r) p[r] = a[r];
+}
+
 // IL (lane-interleaved rows): the R rows of a thread are 32 apart (row warp_k0 + lane + 32 r), so
 // one gather instruction covers 32 consecutive rows; val/col then take R scalar loads per slot.
 template <bool IL, typename T, int R>
@@ -316,6 +336,11 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const uint64_t pol_s = make_policy(pol & 0xff);
   const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
   row_chains<T, Off, R, U, PIPE, IL, WIN>(acc, val, col, s_cs, col_start, k0, len, x, s_win, win_shift, pol_s, pol_x);
+  const int y_kind = (pol >> 16) & 0xff;
+  if ((MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) && !IL && R > 1 && y_kind && k0 + R <= n) {
+    // (the Lanczos product's y is read by the next pass: no evict-first there)
+    st_rows<T, R>(y + k0, acc, make_policy(MODE == STORE_DIRECT_DOT ? 0 : y_kind - 1));
+  } else
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t k = k0 + r * RS;
@@ -500,7 +525,7 @@ pjds_spmv_split_kernel(const T* __restrict__ val, const int* __restrict__ col, c
   }
 }
 
-static int g_pol = 1 | (2 << 8);  // val/col evict_first, x evict_last
+static int g_pol = 1 | (2 << 8) | (2 << 16);  // val/col evict_first, x evict_last, y vector store evict_first
 static int g_tile_order = 2;  // 0 storage order, 1 by first row's original index, 2 auto (see launch_pjds_t)
 
 // Tiles (CTAs of rows_per_tile consecutive sorted rows) ordered by the original index of their first
@@ -846,9 +871,13 @@ int set_tile_order(int mode) { return set_tile_order_impl(mode); }
 int set_schedule(int mode) { return set_schedule_impl(mode); }
 
 int set_cache_policy(int stream_kind, int x_kind) {
-  if (stream_kind < 0 || stream_kind > 3 || x_kind < 0 || x_kind > 3)
+  // bits 8-15 of stream_kind: y store of the permuted-basis kernel (0 plain scalar stores,
+  // 1 + kind: one R-wide vector store with that L2 policy; default 2 = vector, evict_first)
+  const int y_kind = (stream_kind >> 8) & 0xff;
+  stream_kind &= 0xff;
+  if (stream_kind > 3 || x_kind < 0 || x_kind > 3 || y_kind > 4)
     return set_error(PJDS_ERR_INVALID_ARG, "cache policy kinds: 0 normal, 1 evict_first, 2 evict_last, 3 unchanged");
-  g_pol = stream_kind | (x_kind << 8);
+  g_pol = stream_kind | (x_kind << 8) | (y_kind << 16);
   return PJDS_OK;
 }
 

@@ -27,7 +27,7 @@ p.add_argument("--dtypes", default="f64,f32")
 p.add_argument("--fmts", default="pjds32,pjds64,pjds128,ellr")
 p.add_argument("--reps", type=int, default=30)
 p.add_argument("--variants", default="0x0")
-p.add_argument("--policies", default="1x2")
+p.add_argument("--policies", default="513x2", help="stream x x; stream bits 8-15 = y store (0 plain, 1+kind vector); 513x2 = the library default")
 p.add_argument("--orders", default="2")
 p.add_argument("--scheds", default="0", help="0 static CTA grid, 1 dynamic warp tiles")
 p.add_argument("--sigmas", default="0")
