@@ -82,8 +82,9 @@ for cfg in a.configs.split(","):
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(a.reps): A.spmv(y, x)
-            ck = clocks()
-            e1.record(); torch.cuda.synchronize()
+            e1.record()
+            ck = clocks()  # after e1 is enqueued: a slow first NVML query must not delay e1 (it did: C2 +28 us)
+            torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
             print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sched": int(sch), "keys": kspec, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
