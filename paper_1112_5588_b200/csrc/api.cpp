@@ -161,16 +161,17 @@ int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream) {
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_host: handle is host-only");
   const size_t bytes_x = (size_t)A->ncols * dtype_size(A->h.dtype), bytes_y = (size_t)A->h.n * dtype_size(A->h.dtype);
   const bool sym = A->direct_store;
+  // symmetric: a second vector each for the basis change, at a 256-byte aligned offset
+  const size_t off_x = ((bytes_x ? bytes_x : 16) + 255) & ~size_t(255), off_y = ((bytes_y ? bytes_y : 16) + 255) & ~size_t(255);
   if (!A->d_xs) {
-    // symmetric: two extra vectors for the basis change before / after the product
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_xs, (bytes_x ? bytes_x : 16) * (sym ? 2 : 1)));
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_ys, (bytes_y ? bytes_y : 16) * (sym ? 2 : 1)));
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_xs, sym ? 2 * off_x : off_x));
+    PJDS_CUDA_TRY(cudaMalloc(&A->d_ys, sym ? 2 * off_y : off_y));
   }
   cudaStream_t s = (cudaStream_t)stream;
   PJDS_CUDA_TRY(cudaMemcpyAsync(A->d_xs, x_host, bytes_x, cudaMemcpyHostToDevice, s));
   if (sym) {  // host vectors are in the ORIGINAL basis: permute once before and once after
-    char* xp = (char*)A->d_xs + (bytes_x ? bytes_x : 16);
-    char* yp = (char*)A->d_ys + (bytes_y ? bytes_y : 16);
+    char* xp = (char*)A->d_xs + off_x;
+    char* yp = (char*)A->d_ys + off_y;
     PJDS_TRY(launch_permute(A->d_perm, A->h.n, A->d_xs, xp, A->h.dtype, 0, s));
     PJDS_TRY(launch_pjds_spmv(A, yp, xp, s, false));
     PJDS_TRY(launch_permute(A->d_perm, A->h.n, yp, A->d_ys, A->h.dtype, 1, s));

@@ -638,9 +638,11 @@ int st;
     if (st != PJDS_OK) return st;
     if (done) return PJDS_OK;
   }
+  // the vector y store needs y aligned to R elements (caller pointers need only T alignment)
+  const int pol = ((uintptr_t)y % (R * sizeof(T))) ? (g_pol & 0xffff) : g_pol;
 #define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
   pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
-      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, g_pol, order, dot_part, h.sigma, \
+      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, pol, order, dot_part, h.sigma, \
       A->d_wcs_off, (const T* const*)A->d_win, A->win_shift)
 #define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
   if (A->d_win) {  // fused remote-gather dist matrix: plain main loop, direct or perm store

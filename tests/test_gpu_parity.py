@@ -391,6 +391,51 @@ def test_tile_order_bitwise(pj, order):
         L.pjds_set_tile_order(2)
 
 
+@pytest.mark.parametrize("y_kind", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [(0, 0), (4, 2), (2, 4), (1, 8)])
+def test_y_store_bitwise(pj, y_kind, variant):
+    """The permuted-basis y store (plain scalar stores, or one R-wide vector store with each L2
+    policy; pjds_set_cache_policy bits 8-15) writes the same chains, ragged last thread included."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_cache_policy(1 | (y_kind << 8), 2) == 0
+        assert L.pjds_set_kernel_variant(*variant) == 0
+        for dtype in (np.float64, np.float32):
+            for n, rp, col, val in (inputs.config_crs("C1"), inputs.small("random", 1501, seed=7, dtype=dtype, max=40)):
+                val = val.astype(dtype)
+                x = inputs.vector(n, dtype)
+                A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+                y = np.empty(n, dtype)
+                A.spmv_host(y, x)
+                check_y(y, n, rp, col, val, x)
+    finally:
+        L.pjds_set_cache_policy(1 | (2 << 8), 2)
+        L.pjds_set_kernel_variant(0, 0)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_y_store_unaligned_output(pj, dtype):
+    """A caller's y needs only element alignment: a tensor view one element into its storage takes
+    the plain-store path instead of faulting on the R-wide vector store."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_kernel_variant(4, 2) == 0
+        n, rp, col, val = inputs.small("random", 1501, seed=8, dtype=dtype, max=40)
+        x = inputs.vector(n, dtype)
+        A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+        tdt = torch.float64 if dtype == np.float64 else torch.float32
+        for shift in (0, 1, 2, 3):
+            buf = torch.full((n + 4,), float("nan"), dtype=tdt, device="cuda")
+            y = buf[shift:shift + n]
+            A.spmv(y, tdev(x[A.export()["perm"]]))
+            torch.cuda.synchronize()
+            yo = np.empty(n, dtype)
+            yo[A.export()["perm"]] = y.cpu().numpy()
+            check_y(yo, n, rp, col, val, x)
+    finally:
+        L.pjds_set_kernel_variant(0, 0)
+
+
 def test_tile_keys_bitwise(pj):
     """pjds_set_tile_keys (user execution order: a random key, the HMEp 2-D window key, and back to
     the default) never changes a row's chain; a wrong-length key is rejected."""
