@@ -291,12 +291,33 @@ enum {
 int pjds_dist_create(pjds_dist_t* out, pjds_plan_t plan, const void* val_loc, int dtype,
                      int32_t block_rows, const int64_t* send_counts, const int32_t* send_cols,
                      int32_t transport, const void* nccl_unique_id, uint32_t flags);
+/*
+ * pjds_dist_create_crs: the one-call collective create of SURVEY §8(b) (NCCL transport; every rank
+ * calls it with the same nranks, n_global, row_offsets, block_rows and flags).
+ *  nccl_unique_id  128-byte ncclUniqueId, identical on every rank (rank 0 makes it with
+ *                  pjds_nccl_unique_id and the caller broadcasts it); unused when nranks == 1
+ *  row_offsets     [nranks+1], rank r owns rows and x entries [row_offsets[r], row_offsets[r+1])
+ *  rowptr_loc      [n_loc+1] CRS row pointers of this rank's rows (rowptr_loc[0] = 0)
+ *  col_global_loc  GLOBAL column ids of this rank's rows;  val_loc: their values (dtype)
+ * Inside: pjds_dist_plan, ncclCommInitRank on the caller's current device, the recv-list ->
+ * send-list exchange as grouped ncclSend/ncclRecv (counts, then ids), and pjds_dist_create on the
+ * same communicator.  Host arrays are copied; the caller keeps ownership.  Errors as
+ * pjds_dist_create (+ PJDS_ERR_NCCL for a failed communicator or exchange); nothing is left
+ * allocated on failure.  Blocks until every rank has joined (a collective).
+ */
+int pjds_dist_create_crs(pjds_dist_t* out, const void* nccl_unique_id, int32_t nranks, int32_t rank,
+                         int64_t n_global, const int64_t* row_offsets, const int64_t* rowptr_loc,
+                         const int32_t* col_global_loc, const void* val_loc, int dtype, int32_t block_rows,
+                         uint32_t flags);
 /* PJDS_TRANSPORT_P2P setup (collective; the caller all-gathers the blobs, e.g. with
    torch.distributed.all_gather_object):
    pjds_dist_p2p_export: writes this rank's fixed-size blob (CUDA IPC handle of its halo/flag region
      and its halo layout) to `blob` (may be NULL to query) and its size to *bytes.
    pjds_dist_p2p_connect: `blobs` = nranks blobs in rank order; opens the peers' regions.
-   pjds_dist_p2p_check: *timed_out = 1 if a flag wait gave up (~10 s) since create (synchronous). */
+   pjds_dist_p2p_check: synchronises the device, then *timed_out = 1 if a bounded flag wait gave up
+     (~10 s) since create or the previous check, and clears the word.  While it is set, every
+     pjds_dist_spmv call of a P2P / DIRECT handle returns PJDS_ERR_CUDA without enqueuing work (the
+     y of the call that timed out is invalid: it ran on a stale halo / window). */
 int pjds_dist_p2p_export(pjds_dist_t D, void* blob, int64_t* bytes);
 int pjds_dist_p2p_connect(pjds_dist_t D, const void* blobs, int64_t blob_bytes);
 int pjds_dist_p2p_check(pjds_dist_t D, int32_t* timed_out);

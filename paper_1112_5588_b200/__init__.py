@@ -97,7 +97,12 @@ class PjdsMatrix:
             pass
 
     def spmv(self, y, x, stream=None):
-        """y = A x on the GPU (torch CUDA tensors of the matrix dtype, original basis)."""
+        """y = A x on the GPU (torch CUDA tensors of the matrix dtype).
+
+        The basis depends on how the handle was built: a row-permuted handle (symmetric=False)
+        takes x and returns y in the ORIGINAL basis; a symmetric=True handle (the paper's permuted
+        basis) takes x and returns y in the PERMUTED basis -- convert once with
+        to_permuted / from_permuted before and after an iterative scheme."""
         call("pjds_spmv", self._h, _check_vec(y, self.n, self.dtype, "y"), _check_vec(x, self.n, self.dtype, "x"),
              _stream_ptr(stream))
         return y
@@ -345,18 +350,30 @@ class DistPjds:
         import torch.distributed as dist
         R, rank = dist.get_world_size(group), dist.get_rank(group)
         val_loc = np.ascontiguousarray(val_loc)
+        if transport == "nccl":
+            # the one-call collective create: the library plans, builds its NCCL
+            # communicator and exchanges the index lists over it; Python only broadcasts the id
+            uid = (ctypes.c_char * 128)()
+            if R > 1:
+                call("pjds_nccl_load", _nccl_path())
+                if rank == 0:
+                    call("pjds_nccl_unique_id", uid)
+                obj = [bytes(uid) if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                ctypes.memmove(uid, obj[0], 128)
+            offs = np.ascontiguousarray(offsets, np.int64)
+            rp = np.ascontiguousarray(rowptr_loc, np.int64)
+            cl = np.ascontiguousarray(col_loc, np.int32)
+            h = ctypes.c_void_p()
+            call("pjds_dist_create_crs", ctypes.byref(h), uid, R, rank, int(n_global), offs.ctypes.data,
+                 rp.ctypes.data, cl.ctypes.data, val_loc.ctypes.data, _dt(val_loc), int(block_rows),
+                 PJDS_PERM_SYMMETRIC if permuted else 0)
+            return cls(h, None, R, rank, _dt(val_loc))
         plan = DistPlan(R, rank, n_global, offsets, rowptr_loc, col_loc)
         rc, rcols = plan.recv()
         sc, scols = exchange_lists(rc, rcols, group)
         uid = (ctypes.c_char * 128)()
-        tr = {"nccl": PJDS_TRANSPORT_NCCL, "p2p": _lib.PJDS_TRANSPORT_P2P, "direct": _lib.PJDS_TRANSPORT_DIRECT}[transport]
-        if R > 1 and transport == "nccl":
-            call("pjds_nccl_load", _nccl_path())
-            if rank == 0:
-                call("pjds_nccl_unique_id", uid)
-            obj = [bytes(uid) if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            ctypes.memmove(uid, obj[0], 128)
+        tr = {"p2p": _lib.PJDS_TRANSPORT_P2P, "direct": _lib.PJDS_TRANSPORT_DIRECT}[transport]
         h = ctypes.c_void_p()
         call("pjds_dist_create", ctypes.byref(h), plan._h, val_loc.ctypes.data, _dt(val_loc), int(block_rows),
              sc.ctypes.data, scols.ctypes.data, tr, uid, PJDS_PERM_SYMMETRIC if permuted else 0)

@@ -89,6 +89,7 @@ _SIGS = {
     "pjds_dist_plan_recv": [c_p, c_p, c_p],
     "pjds_dist_plan_destroy": [c_p],
     "pjds_dist_create": [c_p, c_p, c_p, ctypes.c_int, c_i32, c_p, c_p, c_i32, c_p, c_u32],
+    "pjds_dist_create_crs": [c_p, c_p, c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, ctypes.c_int, c_i32, c_u32],
     "pjds_dist_permute": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_dist_spmv": [c_p, c_p, c_p, c_p, c_u32],
     "pjds_dist_group_spmv": [c_p, c_i32, c_p, c_p, c_p, c_u32],

@@ -139,11 +139,8 @@ int pjds_create_from_crs_ex(pjds_t* out, int64_t n, const int64_t* rowptr, const
 int pjds_destroy(pjds_t A) {
   if (!A) return PJDS_OK;
   if (A->on_device) {
-    int prev = -1;
-    cudaGetDevice(&prev);
-    if (A->device >= 0) cudaSetDevice(A->device);
+    DeviceGuard dg(A->device);
     free_pjds_device(A);
-    if (prev >= 0) cudaSetDevice(prev);
   }
   delete A;
   return PJDS_OK;
@@ -153,7 +150,55 @@ int pjds_spmv(pjds_t A, void* y, const void* x, void* stream) {
   if (!A || (A->h.n > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: NULL argument");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: handle is host-only");
   if (y == x && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv: y aliases x");
+  DeviceGuard dg(A->device);
   return launch_pjds_spmv(A, y, x, (cudaStream_t)stream, false);
+}
+
+// Staging of pjds_spmv_host / pjds_spmv_host_batch is all-or-nothing: on any failure everything
+// created so far is released and the pointers are reset, so a later call retries from scratch
+// instead of launching on a half-allocated set.
+static void free_host_staging(pjds_mat* A) {
+  cudaFree(A->d_xs); cudaFree(A->d_ys);
+  A->d_xs = A->d_ys = nullptr;
+}
+static void free_batch_staging(pjds_mat* A) {
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(A->d_bx[b]); cudaFree(A->d_by[b]); cudaFree(A->d_bp[b]);
+    A->d_bx[b] = A->d_by[b] = A->d_bp[b] = nullptr;
+  }
+  if (A->s_h2d) cudaStreamDestroy(A->s_h2d);
+  if (A->s_d2h) cudaStreamDestroy(A->s_d2h);
+  A->s_h2d = A->s_d2h = nullptr;
+  for (auto& e : A->ev_b) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
+}
+static int alloc_host_staging(pjds_mat* A, size_t bx, size_t by) {
+  if (A->d_xs && A->d_ys) return PJDS_OK;
+  free_host_staging(A);
+  if (cudaMalloc(&A->d_xs, bx) != cudaSuccess || cudaMalloc(&A->d_ys, by) != cudaSuccess) {
+    cudaGetLastError();
+    free_host_staging(A);
+    return set_error(PJDS_ERR_OOM, "pjds_spmv_host: staging allocation failed");
+  }
+  return PJDS_OK;
+}
+static int alloc_batch_staging(pjds_mat* A, size_t bx, size_t by, bool sym) {
+  bool ok = true;
+  for (int b = 0; b < 2 && ok; ++b) {
+    ok = cudaMalloc(&A->d_bx[b], bx) == cudaSuccess && cudaMalloc(&A->d_by[b], by) == cudaSuccess &&
+         (!sym || cudaMalloc(&A->d_bp[b], std::max(bx, by)) == cudaSuccess);
+  }
+  ok = ok && cudaStreamCreateWithFlags(&A->s_h2d, cudaStreamNonBlocking) == cudaSuccess &&
+       cudaStreamCreateWithFlags(&A->s_d2h, cudaStreamNonBlocking) == cudaSuccess;
+  for (auto& e : A->ev_b) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    free_batch_staging(A);
+    return set_error(PJDS_ERR_OOM, "pjds_spmv_host_batch: staging allocation failed");
+  }
+  return PJDS_OK;
 }
 
 int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream) {
@@ -163,10 +208,8 @@ int pjds_spmv_host(pjds_t A, void* y_host, const void* x_host, void* stream) {
   const bool sym = A->direct_store;
   // symmetric: a second vector each for the basis change, at a 256-byte aligned offset
   const size_t off_x = ((bytes_x ? bytes_x : 16) + 255) & ~size_t(255), off_y = ((bytes_y ? bytes_y : 16) + 255) & ~size_t(255);
-  if (!A->d_xs) {
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_xs, sym ? 2 * off_x : off_x));
-    PJDS_CUDA_TRY(cudaMalloc(&A->d_ys, sym ? 2 * off_y : off_y));
-  }
+  DeviceGuard dg(A->device);
+  PJDS_TRY(alloc_host_staging(A, sym ? 2 * off_x : off_x, sym ? 2 * off_y : off_y));
   cudaStream_t s = (cudaStream_t)stream;
   PJDS_CUDA_TRY(cudaMemcpyAsync(A->d_xs, x_host, bytes_x, cudaMemcpyHostToDevice, s));
   if (sym) {  // host vectors are in the ORIGINAL basis: permute once before and once after
@@ -190,16 +233,8 @@ int pjds_spmv_host_batch(pjds_t A, void* const* y_host, const void* const* x_hos
   const size_t vs = dtype_size(A->h.dtype);
   const size_t bx = std::max<size_t>((size_t)A->ncols * vs, 16), by = std::max<size_t>((size_t)A->h.n * vs, 16);
   const bool sym = A->direct_store;
-  if (!A->d_bx[0]) {
-    for (int b = 0; b < 2; ++b) {
-      PJDS_CUDA_TRY(cudaMalloc(&A->d_bx[b], bx));
-      PJDS_CUDA_TRY(cudaMalloc(&A->d_by[b], by));
-      if (sym) PJDS_CUDA_TRY(cudaMalloc(&A->d_bp[b], std::max(bx, by)));
-    }
-    PJDS_CUDA_TRY(cudaStreamCreateWithFlags(&A->s_h2d, cudaStreamNonBlocking));
-    PJDS_CUDA_TRY(cudaStreamCreateWithFlags(&A->s_d2h, cudaStreamNonBlocking));
-    for (auto& e : A->ev_b) PJDS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
+  DeviceGuard dg(A->device);
+  if (!A->ev_b[8]) PJDS_TRY(alloc_batch_staging(A, bx, by, sym));  // the last object created
   cudaStream_t cs = (cudaStream_t)stream;
   cudaEvent_t *ev_x = A->ev_b, *ev_y = A->ev_b + 2, *ev_xf = A->ev_b + 4, *ev_yf = A->ev_b + 6, ev0 = A->ev_b[8];
   // the copy streams start after everything already queued on the caller's stream
@@ -238,6 +273,7 @@ int pjds_permute(pjds_t A, void* dst, const void* src, int32_t direction, void* 
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: handle is host-only");
   if (dst == src && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: dst aliases src");
   if (direction != 0 && direction != 1) return set_error(PJDS_ERR_INVALID_ARG, "pjds_permute: direction 0 or 1");
+  DeviceGuard dg(A->device);
   return launch_permute(A->d_perm, A->h.n, src, dst, A->h.dtype, direction, (cudaStream_t)stream);
 }
 
@@ -332,6 +368,7 @@ int ellr_create_from_crs(ellr_t* out, int64_t n, const int64_t* rowptr, const in
 int ellr_destroy(ellr_t A) {
   if (!A) return PJDS_OK;
   if (A->on_device) {
+    DeviceGuard dg(A->device);
     cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_rowmax);
   }
   delete A;
@@ -342,6 +379,7 @@ int ellr_spmv(ellr_t A, void* y, const void* x, void* stream) {
   if (!A || (A->h.n > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: NULL argument");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: handle is host-only");
   if (y == x && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "ellr_spmv: y aliases x");
+  DeviceGuard dg(A->device);
   return launch_ellr_spmv(A, y, x, (cudaStream_t)stream);
 }
 
@@ -425,12 +463,8 @@ int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n) {
   if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: NULL handle");
   if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: handle is host-only");
   if (key && n != A->h.n) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: need one key per row");
-  int prev = -1;
-  cudaGetDevice(&prev);
-  if (A->device >= 0) cudaSetDevice(A->device);
-  const int s = build_tile_orders(A, key);
-  if (prev >= 0) cudaSetDevice(prev);
-  return s;
+  DeviceGuard dg(A->device);
+  return build_tile_orders(A, key);
 }
 
 int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gbs) {

@@ -172,7 +172,11 @@ struct pjds_dist {
   std::vector<int64_t> offsets;                 // row offsets [R+1]
   uint64_t* ready_flags() const { return (uint64_t*)(p2p_region + p2p_flags_off); }
   uint64_t* done_flags() const { return ready_flags() + R; }
-  unsigned* err_flag() const { return (unsigned*)(done_flags() + R); }
+  // timeout word of the bounded peer waits: pinned, mapped host memory, so that every
+  // pjds_dist_spmv call can see a timeout of an earlier call without a device synchronisation
+  unsigned* h_err = nullptr;
+  unsigned* d_h_err = nullptr;                  // device alias of h_err
+  unsigned* err_flag() const { return d_h_err; }
 };
 
 namespace {
@@ -195,12 +199,21 @@ int post_nccl(pjds_dist* D, const void* x_loc, cudaStream_t s) {
   return PJDS_OK;
 }
 
+static int alloc_err_word(pjds_dist* D) {
+  if (D->h_err) return PJDS_OK;
+  PJDS_CUDA_TRY(cudaHostAlloc((void**)&D->h_err, 64, cudaHostAllocMapped));
+  *(volatile unsigned*)D->h_err = 0;
+  PJDS_CUDA_TRY(cudaHostGetDevicePointer((void**)&D->d_h_err, D->h_err, 0));
+  return PJDS_OK;
+}
+
 // P2P transport: allocate the IPC-exported region and the per-call device tables.
 int p2p_setup(pjds_dist* D, const std::vector<int32_t>& ids, const std::vector<int64_t>& seg) {
   const size_t vs = vsz(D);
   D->p2p_halo_bytes = (std::max<size_t>(D->halo * vs, 16) + 255) / 256 * 256;
   D->p2p_region_bytes = 2 * D->p2p_halo_bytes + 2 * (size_t)D->R * 8 + 256;
   D->p2p_flags_off = 2 * D->p2p_halo_bytes;
+  PJDS_TRY(alloc_err_word(D));
   PJDS_CUDA_TRY(cudaMalloc(&D->p2p_region, D->p2p_region_bytes));
   PJDS_CUDA_TRY(cudaMemset(D->p2p_region, 0, D->p2p_region_bytes));
   const size_t ns = D->send_peers.size(), nr = D->recv_peers.size();
@@ -227,6 +240,7 @@ int direct_setup(pjds_dist* D) {
   const size_t win = (std::max<size_t>(D->n_loc * vs, 16) + 255) / 256 * 256;
   D->p2p_flags_off = win;
   D->p2p_region_bytes = win + 2 * (size_t)D->R * 8 + 256;
+  PJDS_TRY(alloc_err_word(D));
   PJDS_CUDA_TRY(cudaMalloc(&D->p2p_region, D->p2p_region_bytes));
   PJDS_CUDA_TRY(cudaMemset(D->p2p_region, 0, D->p2p_region_bytes));
   const size_t ns = D->send_peers.size(), nr = D->recv_peers.size();
@@ -375,34 +389,140 @@ int pjds_dist_plan_destroy(pjds_plan_t P) {
 
 int pjds_dist_destroy(pjds_dist_t D);
 
+static int dist_create_impl(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype, int32_t block_rows,
+                            const int64_t* send_counts, const int32_t* send_cols, int32_t transport,
+                            const void* nccl_id, uint32_t flags, ncclComm_t comm_in);
+
 int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype, int32_t block_rows,
                      const int64_t* send_counts, const int32_t* send_cols, int32_t transport, const void* nccl_id,
                      uint32_t flags) {
-  if (!out || !P) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: NULL argument");
+  return dist_create_impl(out, P, val, dtype, block_rows, send_counts, send_cols, transport, nccl_id, flags, nullptr);
+}
+
+// One-call collective create (SURVEY §8(b) signature): NCCL communicator from the unique id, the
+// plan, the recv-list -> send-list exchange over that communicator (counts, then ids, as grouped
+// point-to-point messages), then the same create as the three-step path on the same communicator.
+int pjds_dist_create_crs(pjds_dist_t* out, const void* nccl_id, int32_t nranks, int32_t rank, int64_t n_global,
+                         const int64_t* row_offsets, const int64_t* rowptr_loc, const int32_t* col_global_loc,
+                         const void* val_loc, int dtype, int32_t block_rows, uint32_t flags) {
+  if (!out) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create_crs: out is NULL");
   *out = nullptr;
-  if (flags & ~(uint32_t)PJDS_PERM_SYMMETRIC) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: unknown flags");
+  if (nranks > 1 && !nccl_id) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create_crs: nccl_unique_id is NULL");
+  pjds_plan_t P = nullptr;
+  PJDS_TRY(pjds_dist_plan(&P, nranks, rank, n_global, row_offsets, rowptr_loc, col_global_loc));
+  ncclComm_t comm = nullptr;
+  cudaStream_t st = nullptr;
+  int64_t* d_cnt = nullptr;  // [2R]: recv counts out, send counts in
+  int32_t* d_ids = nullptr;  // [halo + send_total]
+  std::vector<int64_t> sc(nranks, 0);
+  std::vector<int32_t> scols;
+  auto cleanup = [&](int status) {
+    if (st) cudaStreamDestroy(st);
+    cudaFree(d_cnt);
+    cudaFree(d_ids);
+    if (status != PJDS_OK && comm) g_nccl.commDestroy(comm);
+    pjds_dist_plan_destroy(P);
+    return status;
+  };
+  if (nranks > 1) {
+    int s = nccl_load(nullptr);
+    if (s != PJDS_OK) return cleanup(s);
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = g_nccl.commInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      comm = nullptr;
+      return cleanup(set_error(PJDS_ERR_NCCL, std::string("ncclCommInitRank: ") + g_nccl.errStr(r)));
+    }
+    const int R = nranks;
+    const int64_t halo = (int64_t)P->recv_cols.size();
+    auto nccl_fail = [&](ncclResult_t rr, const char* what) {
+      return cleanup(set_error(PJDS_ERR_NCCL, std::string(what) + ": " + g_nccl.errStr(rr)));
+    };
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&d_cnt, 2 * R * 8) != cudaSuccess ||
+        cudaMemcpy(d_cnt, P->recv_counts.data(), R * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return cleanup(set_error(PJDS_ERR_CUDA, "pjds_dist_create_crs: count buffers"));
+    // 1. counts: my recv count from q goes to q, q's recv count from me comes back as my send count
+    ncclResult_t rr;
+    if ((rr = g_nccl.groupStart()) != ncclSuccess) return nccl_fail(rr, "ncclGroupStart");
+    for (int q = 0; q < R; ++q) {
+      if (q == rank) continue;
+      if ((rr = g_nccl.send(d_cnt + q, 1, ncclInt64, q, comm, st)) != ncclSuccess) return nccl_fail(rr, "ncclSend");
+      if ((rr = g_nccl.recv(d_cnt + R + q, 1, ncclInt64, q, comm, st)) != ncclSuccess) return nccl_fail(rr, "ncclRecv");
+    }
+    if ((rr = g_nccl.groupEnd()) != ncclSuccess) return nccl_fail(rr, "ncclGroupEnd");
+    if (cudaStreamSynchronize(st) != cudaSuccess ||
+        cudaMemcpy(sc.data(), d_cnt + R, R * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return cleanup(set_error(PJDS_ERR_CUDA, "pjds_dist_create_crs: count exchange"));
+    sc[rank] = 0;
+    int64_t send_total = 0;
+    for (int q = 0; q < R; ++q) {
+      if (sc[q] < 0) return cleanup(set_error(PJDS_ERR_NCCL, "pjds_dist_create_crs: negative count received"));
+      send_total += sc[q];
+    }
+    // 2. ids: my recv list from q goes to q and becomes q's send list to me
+    if (cudaMalloc(&d_ids, std::max<int64_t>(halo + send_total, 1) * 4) != cudaSuccess ||
+        (halo && cudaMemcpy(d_ids, P->recv_cols.data(), halo * 4, cudaMemcpyHostToDevice) != cudaSuccess))
+      return cleanup(set_error(PJDS_ERR_OOM, "pjds_dist_create_crs: id buffers"));
+    if ((rr = g_nccl.groupStart()) != ncclSuccess) return nccl_fail(rr, "ncclGroupStart");
+    int64_t ro = 0, so = halo;
+    for (int q = 0; q < R; ++q) {
+      const int64_t rc = P->recv_counts[q];
+      if (rc && (rr = g_nccl.send(d_ids + ro, (size_t)rc, ncclInt32, q, comm, st)) != ncclSuccess)
+        return nccl_fail(rr, "ncclSend");
+      if (sc[q] && (rr = g_nccl.recv(d_ids + so, (size_t)sc[q], ncclInt32, q, comm, st)) != ncclSuccess)
+        return nccl_fail(rr, "ncclRecv");
+      ro += rc;
+      so += sc[q];
+    }
+    if ((rr = g_nccl.groupEnd()) != ncclSuccess) return nccl_fail(rr, "ncclGroupEnd");
+    scols.resize(send_total);
+    if (cudaStreamSynchronize(st) != cudaSuccess ||
+        (send_total && cudaMemcpy(scols.data(), d_ids + halo, send_total * 4, cudaMemcpyDeviceToHost) != cudaSuccess))
+      return cleanup(set_error(PJDS_ERR_CUDA, "pjds_dist_create_crs: id exchange"));
+  }
+  const int s = dist_create_impl(out, P, val_loc, dtype, block_rows, sc.data(), scols.data(), PJDS_TRANSPORT_NCCL,
+                                 nullptr, flags, comm);
+  comm = nullptr;  // dist_create_impl took ownership (and destroyed it on failure)
+  return cleanup(s);
+}
+
+static int dist_create_impl(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype, int32_t block_rows,
+                            const int64_t* send_counts, const int32_t* send_cols, int32_t transport,
+                            const void* nccl_id, uint32_t flags, ncclComm_t comm_in) {
+  // comm_in (optional): an NCCL communicator this call takes ownership of, also on failure
+  auto drop_comm = [&](int st) {
+    if (comm_in) g_nccl.commDestroy(comm_in);
+    return st;
+  };
+  if (!out || !P) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: NULL argument"));
+  *out = nullptr;
+  if (flags & ~(uint32_t)PJDS_PERM_SYMMETRIC) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_create: unknown flags"));
   const bool sym = flags & PJDS_PERM_SYMMETRIC;
-  if (dtype != PJDS_F32 && dtype != PJDS_F64) return set_error(PJDS_ERR_INVALID_ARG, "bad dtype");
+  if (dtype != PJDS_F32 && dtype != PJDS_F64) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "bad dtype"));
   if (transport != PJDS_TRANSPORT_NCCL && transport != PJDS_TRANSPORT_LOCAL && transport != PJDS_TRANSPORT_P2P &&
       transport != PJDS_TRANSPORT_DIRECT)
-    return set_error(PJDS_ERR_INVALID_ARG, "bad transport");
-  if (P->nnz_loc > 0 && !val) return set_error(PJDS_ERR_INVALID_ARG, "val is NULL");
-  if (P->R > 1 && !send_counts) return set_error(PJDS_ERR_INVALID_ARG, "send_counts is NULL");
+    return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "bad transport"));
+  if (P->nnz_loc > 0 && !val) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "val is NULL"));
+  if (P->R > 1 && !send_counts) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "send_counts is NULL"));
   if (block_rows == 0) block_rows = 32;
   const int R = P->R;
   int64_t send_total = 0;
   for (int q = 0; q < R && send_counts; ++q) {
-    if (send_counts[q] < 0) return set_error(PJDS_ERR_INVALID_ARG, "negative send count");
-    if (q == P->rank && send_counts[q] != 0) return set_error(PJDS_ERR_INVALID_ARG, "send to self");
+    if (send_counts[q] < 0) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "negative send count"));
+    if (q == P->rank && send_counts[q] != 0) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "send to self"));
     send_total += send_counts[q];
   }
-  if (send_total > 0 && !send_cols) return set_error(PJDS_ERR_INVALID_ARG, "send_cols is NULL");
+  if (send_total > 0 && !send_cols) return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "send_cols is NULL"));
   for (int64_t i = 0; i < send_total; ++i)
     if (send_cols[i] < P->lo || send_cols[i] >= P->hi)
-      return set_error(PJDS_ERR_INVALID_ARG, "send_cols entry not owned by this rank");
+      return drop_comm(set_error(PJDS_ERR_INVALID_ARG, "send_cols entry not owned by this rank"));
 
   pjds_dist* D = new (std::nothrow) pjds_dist();
-  if (!D) return set_error(PJDS_ERR_OOM, "dist allocation failed");
+  if (!D) return drop_comm(set_error(PJDS_ERR_OOM, "dist allocation failed"));
+  D->nccl = comm_in;  // owned by the handle from here on (pjds_dist_destroy releases it)
+  comm_in = nullptr;
   D->R = R; D->rank = P->rank; D->transport = transport; D->dtype = dtype;
   D->n_loc = P->n_loc; D->halo = (int64_t)P->recv_cols.size(); D->send_total = send_total;
   D->nnz_loc_part = (int64_t)P->loc_col.size(); D->nnz_nl_part = (int64_t)P->nl_col.size();
@@ -578,7 +698,7 @@ int pjds_dist_create(pjds_dist_t* out, pjds_plan_t P, const void* val, int dtype
       cudaEventCreateWithFlags(&D->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&D->ev_comm, cudaEventDisableTiming) != cudaSuccess)
     return fail(set_error(PJDS_ERR_CUDA, "stream/event creation failed"));
-  if (transport == PJDS_TRANSPORT_NCCL && R > 1) {
+  if (transport == PJDS_TRANSPORT_NCCL && R > 1 && !D->nccl) {
     if (!nccl_id) return fail(set_error(PJDS_ERR_INVALID_ARG, "nccl_unique_id is NULL"));
     if ((s = nccl_load(nullptr)) != PJDS_OK) return fail(s);
     ncclUniqueId id;
@@ -605,6 +725,8 @@ int pjds_dist_destroy(pjds_dist_t D) {
   cudaFree(D->d_send_peers); cudaFree(D->d_recv_peers);
   cudaFree(D->d_dst[0]); cudaFree(D->d_dst[1]); cudaFree(D->d_ready_targets); cudaFree(D->d_done_targets);
   cudaFree(D->d_win);
+  if (D->h_err) cudaFreeHost(D->h_err);
+  D->h_err = D->d_h_err = nullptr;
   pjds_destroy(D->A_loc);
   pjds_destroy(D->A_nl);
   delete D;
@@ -768,9 +890,12 @@ int pjds_dist_p2p_check(pjds_dist_t D, int32_t* timed_out) {
     *timed_out = 0;
     return PJDS_OK;
   }
-  unsigned e = 0;
-  PJDS_CUDA_TRY(cudaMemcpy(&e, D->err_flag(), sizeof(e), cudaMemcpyDeviceToHost));
-  *timed_out = (int32_t)e;
+  // every wait enqueued so far has finished (or given up) before the word is read; reading it
+  // clears it, so a caller that has handled a timeout can continue
+  PJDS_CUDA_TRY(cudaDeviceSynchronize());
+  volatile unsigned* w = D->h_err;
+  *timed_out = w ? (int32_t)*w : 0;
+  if (w) *w = 0;
   return PJDS_OK;
 }
 
@@ -819,6 +944,9 @@ int pjds_dist_spmv(pjds_dist_t D, void* y, const void* x, void* stream, uint32_t
   if (y == x && D->n_loc > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_dist_spmv: y aliases x");
   if (D->transport == PJDS_TRANSPORT_LOCAL) return set_error(PJDS_ERR_INVALID_ARG, "use pjds_dist_group_spmv for LOCAL transport");
   cudaStream_t s = (cudaStream_t)stream;
+  if (D->h_err && *(volatile unsigned*)D->h_err)
+    return set_error(PJDS_ERR_CUDA, "pjds_dist_spmv: a bounded peer wait of an earlier call timed out (its y is "
+                                    "invalid); pjds_dist_p2p_check reports and clears it");
   const bool comm_needed = D->R > 1 && (!D->sends.empty() || !D->recvs.empty());
   const bool tr = flags & PJDS_TRACE;
   if (tr && !D->tev[0])

@@ -26,6 +26,23 @@ inline int ok() { return PJDS_OK; }
 
 inline size_t dtype_size(int dt) { return dt == PJDS_F64 ? 8 : 4; }
 
+// Makes the handle's device current for the scope of an entry point and restores the caller's
+// device afterwards (handles may be used from any current device; launches and allocations must
+// land on the device that owns the handle's memory).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0 || cudaGetDevice(&prev) != cudaSuccess) { prev = -1; return; }
+    if (prev == dev) prev = -1;
+    else cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 // ---- host-side pJDS arrays (conversion result) ---------------------------------------------
 struct PjdsHost {
   int64_t n = 0, ncols = 0, nnz = 0, n_pad = 0, n_blocks = 0, stored = 0;

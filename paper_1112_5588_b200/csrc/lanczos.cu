@@ -293,6 +293,7 @@ int pjds_lanczos(pjds_t A, const void* v0, int32_t m, double* alpha, double* bet
   if (!A->on_device) return pjds::set_error(PJDS_ERR_INVALID_ARG, "pjds_lanczos: handle is host-only");
   if (!(A->flags & PJDS_PERM_SYMMETRIC))
     return pjds::set_error(PJDS_ERR_INVALID_ARG, "pjds_lanczos: needs a PJDS_PERM_SYMMETRIC (permuted-basis) handle");
+  pjds::DeviceGuard dg(A->device);
   return pjds::lanczos(A, v0, m, alpha, beta, steps_done, (cudaStream_t)stream);
 }
 
