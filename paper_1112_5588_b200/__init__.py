@@ -74,6 +74,11 @@ class PjdsMatrix:
         self.n = self.info["n"]
         self.dtype = self.info["dtype"]
 
+    @property
+    def symmetric(self) -> bool:
+        """True for a permuted-basis handle (PJDS_PERM_SYMMETRIC): spmv takes and returns permuted vectors."""
+        return bool(self.info["flags"] & PJDS_PERM_SYMMETRIC)
+
     @classmethod
     def from_crs(cls, n, rowptr, col, val, block_rows: int = 32, symmetric: bool = False, host_only: bool = False,
                  sigma: int = 0):

@@ -930,9 +930,13 @@ int launch_ellr_t(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
 template <typename T>
 int launch_ellr_dt(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
   int R = g_var_r;
-  if (R == 0) {  // same rule as the pJDS kernel (measured: R=4,U=2 best on C2/C3/C5 in SP and DP)
+  if (R == 0) {
+    // ELLPACK-R's own sweep (profiles/r01_kbench_ellr_variants.jsonl): R=4,U=2 is fastest on
+    // C2/C3/C5 in SP and DP and on the DLR1-shaped C4 in DP (114.9 vs 127.3 us at R=2, 178.8 at
+    // R=1); C4 SP keeps R=2 (68.2 vs 76.1 us at R=4)
     const int64_t np = A->h.n_pad;
-    R = np / 4 >= (int64_t(1) << 19) ? 4 : (np / 2 >= (int64_t(1) << 17) ? 2 : 1);
+    const int64_t r4_rows = sizeof(T) == 8 ? (int64_t(1) << 16) : (int64_t(1) << 19);
+    R = np / 4 >= r4_rows ? 4 : (np / 2 >= (int64_t(1) << 17) ? 2 : 1);
   }
   if (R == 4) return launch_ellr_t<T, 4, 2>(A, y, x, s);
   if (R == 2) return launch_ellr_t<T, 2, 4>(A, y, x, s);

@@ -107,6 +107,17 @@ def test_configs_full(pj, name, dtype):
         torch.cuda.synchronize()
         check_y(y.cpu().numpy(), n, rp, col, val, x)
         del A
+    # the bench's basis: x permuted once, y in the permuted basis, direct
+    # vector store; automatic variant and tile order as bench.py / per_config launch them
+    for br in (32, 128):
+        A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, symmetric=True)
+        xp = A.to_permuted(torch.empty_like(xt), xt)
+        yp = torch.full((n,), float("nan"), dtype=xt.dtype, device="cuda")
+        A.spmv(yp, xp)
+        y = A.from_permuted(torch.empty_like(yp), yp)
+        torch.cuda.synchronize()
+        check_y(y.cpu().numpy(), n, rp, col, val, x)
+        del A
     E = pj.EllrMatrix.from_crs(n, rp, col, val)
     y = torch.empty(n, dtype=xt.dtype, device="cuda")
     E.spmv(y, xt)
@@ -114,8 +125,36 @@ def test_configs_full(pj, name, dtype):
     check_y(y.cpu().numpy(), n, rp, col, val, x)
 
 
+def c5_sampled_rows(g, n, rp):
+    """>= 100 K sampled C5 rows: 100 random chunks of 1000 consecutive rows (all length classes of a
+    region, i.e. whole CTA tiles of several lengths) + 20 K uniformly random rows + first/last."""
+    rng = np.random.default_rng(5)
+    starts = rng.integers(0, n - 1000, 100)
+    rows = np.unique(np.concatenate([(starts[:, None] + np.arange(1000)[None, :]).ravel(),
+                                     rng.integers(0, n, 20000), [0, n - 1]]))
+    return rows
+
+
+def oracle_of_rows(g, rows, rp, dtype):
+    """The sampled rows regenerated from inputs/ as one CRS (the oracle's own copy)."""
+    lens = np.diff(rp)
+    srp = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(lens[rows], out=srp[1:])
+    sc = np.empty(srp[-1], np.int32)
+    sv = np.empty(srp[-1], dtype)
+    # contiguous runs of sampled rows are generated in one call each
+    brk = np.nonzero(np.diff(rows) != 1)[0] + 1
+    for run in np.split(np.arange(len(rows)), brk):
+        r0, r1 = int(rows[run[0]]), int(rows[run[-1]]) + 1
+        _, cc, vv = g.crs(r0, r1, dtype=dtype)
+        sc[srp[run[0]]:srp[run[-1] + 1]] = cc
+        sv[srp[run[0]]:srp[run[-1] + 1]] = vv
+    return srp, sc, sv
+
+
 def test_c5_sampled(pj):
-    """C5 (bench workload, 942 M nnz) in the bench's launch configuration: sampled rows vs the oracle."""
+    """C5 (bench workload, 942 M nnz) in the ORIGINAL basis (row-only permutation, y stored through
+    perm: the §8 default basis, bench compare leg `pjds_rows_only`): sampled rows vs the oracle."""
     g = inputs.Generator.from_config("C5")
     rp, col, val = g.crs()
     n = g.n
@@ -143,6 +182,39 @@ def test_c5_sampled(pj):
     assert np.array_equal(yh[rows], oracle.spmv_chain(len(rows), srp, sc, sv, x))
     # property at full size: y is finite everywhere
     assert np.isfinite(yh).all()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_c5_permuted_bench_instance(pj, dtype):
+    """The exact headline instance of bench.py: C5, permuted basis (PJDS_PERM_SYMMETRIC), b_r = 32,
+    automatic variant (R = 4, U = 2), automatic tile order (original-row order: x > 64 MB), vector
+    y store.  >= 100 K sampled rows against O1 at the O2 bound AND bitwise against the O3 chain (one
+    FMA chain per row in CRS order, Listing 2); all rows finite."""
+    g = inputs.Generator.from_config("C5")
+    rp, col, val = g.crs(dtype=dtype)
+    n = g.n
+    x = inputs.vector(n, dtype)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=32, symmetric=True)
+    del col, val
+    assert A.symmetric
+    xt = tdev(x)
+    xp = A.to_permuted(torch.empty_like(xt), xt)
+    yp = torch.full((n,), float("nan"), dtype=xt.dtype, device="cuda")
+    for _ in range(2):  # the bench times back-to-back launches on the same x / y
+        A.spmv(yp, xp)
+    y = A.from_permuted(torch.empty_like(yp), yp)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(y).all())
+    rows = c5_sampled_rows(g, n, rp)
+    assert len(rows) >= 100_000
+    yh = y.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    srp, sc, sv = oracle_of_rows(g, rows, rp, dtype)
+    y_ref, bound = oracle.spmv_ld(len(rows), srp, sc, sv, x)
+    ok = oracle.acceptance(yh, y_ref, bound, np.diff(srp), dtype)
+    assert ok.all(), f"{(~ok).sum()} sampled rows outside O2"
+    chain = oracle.spmv_chain(len(rows), srp, sc, sv, x)
+    bad = np.nonzero(yh != chain)[0]
+    assert len(bad) == 0, f"{len(bad)} sampled rows differ from the O3 chain, first {rows[bad[:5]]}"
 
 
 def test_spmv_host_e2e(pj):
