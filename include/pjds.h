@@ -96,6 +96,10 @@ int pjds_destroy(pjds_t A);
  * PJDS_PERM_ROWS: x, y original basis.  PJDS_PERM_SYMMETRIC: x, y permuted basis.
  */
 int pjds_spmv(pjds_t A, void* y, const void* x, void* stream);
+/* y[perm[k]] += (A x)_k for a row-permuted handle: y = y + A x, each row's chain from +0.0 added to
+   y_i with ONE rounding add (the dist nonlocal pass, "written twice"; reading 25).
+   Same arguments as pjds_spmv.  PJDS_ERR_UNSUPPORTED for PJDS_PERM_SYMMETRIC handles. */
+int pjds_spmv_accum(pjds_t A, void* y, const void* x, void* stream);
 
 /*
  * pjds_permute — basis change for the permuted-basis mode ("permutation of
@@ -429,10 +433,17 @@ int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n);
 /* Tuning knob (process-wide): L2 eviction priority of the pJDS kernel's streamed val/col loads
    and of its x gathers; kinds 0 evict_normal, 1 evict_first, 2 evict_last, 3 evict_unchanged.
    Bits 8-15 of stream_kind select the y store of the permuted-basis kernel: 0 = plain scalar
-   stores, 1 + kind = one R-wide vector store per thread with that L2 kind.  Default: stream 1,
-   x 2, y 2 (vector, evict_first; the Lanczos product keeps evict_normal for its y).  Results are
-   unaffected. */
+   stores, 1 + kind = one R-wide vector store per thread with that L2 kind.  Bits 16-23 select the
+   scattered stores through perm (row-only basis y[perm[k]], dist nonlocal y +=): 0 = plain
+   (default), 1 + kind = L1::no_allocate store (and load, for +=) with that L2 kind.  Default:
+   stream 1, x 2, y 2 (vector, evict_first; the Lanczos product keeps evict_normal for its y),
+   perm stores plain.  Results are unaffected. */
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind);
+/* Per-handle override of the permuted-basis y store (the policy part of stream_kind bits 8-15
+   above): -1 = follow pjds_set_cache_policy (default); 0 = plain scalar stores; 1 + kind = one
+   R-wide vector store with L2 policy `kind`.  Used for a dist A_loc, whose y the nonlocal pass
+   reads again (an evict-first store would send it to DRAM first).  Results are unchanged. */
+int pjds_set_y_store(pjds_t A, int32_t kind);
 
 /* Tuning knob (process-wide): execution order of the pJDS kernel's CTA tiles.  0 = storage
    order (longest blocks first); 1 = tiles ordered by the original index of their first row, so

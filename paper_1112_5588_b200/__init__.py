@@ -112,6 +112,12 @@ class PjdsMatrix:
              _stream_ptr(stream))
         return y
 
+    def spmv_accum(self, y, x, stream=None):
+        """y += A x (row-permuted handles; one rounding add per row, the dist nonlocal pass)."""
+        call("pjds_spmv_accum", self._h, _check_vec(y, self.n, self.dtype, "y"), _check_vec(x, self.n, self.dtype, "x"),
+             _stream_ptr(stream))
+        return y
+
     def to_permuted(self, dst, src, stream=None):
         """dst[k] = src[perm[k]] on the GPU (basis change before an iterative scheme)."""
         call("pjds_permute", self._h, _check_vec(dst, self.n, self.dtype, "dst"), _check_vec(src, self.n, self.dtype, "src"),

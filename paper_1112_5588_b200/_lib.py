@@ -70,6 +70,7 @@ _SIGS = {
     "pjds_export_windows": [c_p, c_p, c_p],
     "pjds_destroy": [c_p],
     "pjds_spmv": [c_p, c_p, c_p, c_p],
+    "pjds_spmv_accum": [c_p, c_p, c_p, c_p],
     "pjds_spmv_host": [c_p, c_p, c_p, c_p],
     "pjds_spmv_host_batch": [c_p, c_p, c_p, c_i32, c_p],
     "pjds_permute": [c_p, c_p, c_p, c_i32, c_p],
@@ -109,6 +110,7 @@ _SIGS = {
     "pjds_bw_probe": [c_i64, c_i32, c_p, c_p],
     "pjds_set_kernel_variant": [c_i32, c_i32],
     "pjds_set_cache_policy": [c_i32, c_i32],
+    "pjds_set_y_store": [c_p, c_i32],
     "pjds_set_tile_order": [c_i32],
     "pjds_set_schedule": [c_i32],
     "pjds_set_tile_keys": [c_p, c_p, c_i64],

@@ -154,6 +154,16 @@ int pjds_spmv(pjds_t A, void* y, const void* x, void* stream) {
   return launch_pjds_spmv(A, y, x, (cudaStream_t)stream, false);
 }
 
+int pjds_spmv_accum(pjds_t A, void* y, const void* x, void* stream) {
+  if (!A || (A->h.n > 0 && (!y || !x))) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_accum: NULL argument");
+  if (!A->on_device) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_accum: handle is host-only");
+  if (y == x && A->h.n > 0) return set_error(PJDS_ERR_INVALID_ARG, "pjds_spmv_accum: y aliases x");
+  if (A->direct_store)
+    return set_error(PJDS_ERR_UNSUPPORTED, "pjds_spmv_accum: permuted-basis (symmetric) handles store y[k] = only");
+  DeviceGuard dg(A->device);
+  return launch_pjds_spmv(A, y, x, (cudaStream_t)stream, true);
+}
+
 // Staging of pjds_spmv_host / pjds_spmv_host_batch is all-or-nothing: on any failure everything
 // created so far is released and the pointers are reset, so a later call retries from scratch
 // instead of launching on a half-allocated set.
@@ -456,6 +466,13 @@ int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll) {
 }
 
 int pjds_set_cache_policy(int32_t stream_kind, int32_t x_kind) { return set_cache_policy(stream_kind, x_kind); }
+
+int pjds_set_y_store(pjds_t A, int32_t kind) {
+  if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_y_store: NULL handle");
+  if (kind < -1 || kind > 4) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_y_store: kind in -1 .. 4");
+  A->y_store = kind;
+  return PJDS_OK;
+}
 int pjds_set_tile_order(int32_t mode) { return set_tile_order(mode); }
 int pjds_set_schedule(int32_t mode) { return set_schedule(mode); }
 

@@ -104,6 +104,10 @@ struct pjds_mat {
   void** d_win = nullptr;
   int win_shift = 0;
   unsigned long long* d_sched = nullptr;  // dynamic warp-tile schedule: {next tile, CTAs done}
+  // y-store override of the permuted-basis kernel for this handle (-1: the global policy; else
+  // 0 plain stores or 1 + L2 policy kind of the vector store), e.g. a dist A_loc whose y the
+  // nonlocal pass reads again
+  int32_t y_store = -1;
 };
 
 struct ellr_mat {

@@ -173,6 +173,24 @@ __device__ __forceinline__ void st_rows(T* p, const T (&a)[R], uint64_t pol) {
     for (int r = 0; r < R; ++r) p[r] = a[r];
 }
 
+// one scattered y element with an L2 policy (row-only basis: y[perm[k]]; dist nonlocal part: y += )
+__device__ __forceinline__ void st_one(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_one(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double ld_one(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_one(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // IL (lane-interleaved rows): the R rows of a thread are 32 apart (row warp_k0 + lane + 32 r), so
 // one gather instruction covers 32 consecutive rows; val/col then take R scalar loads per slot.
 template <bool IL, typename T, int R>
@@ -337,6 +355,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
   row_chains<T, Off, R, U, PIPE, IL, WIN>(acc, val, col, s_cs, col_start, k0, len, x, s_win, win_shift, pol_s, pol_x);
   const int y_kind = (pol >> 16) & 0xff;
+  const int p_kind = (pol >> 24) & 0x7f;  // scattered stores through perm: 0 plain, 1 + L2 policy kind
   if ((MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) && !IL && R > 1 && y_kind && k0 + R <= n) {
     // (the Lanczos product's y is read by the next pass: no evict-first there)
     st_rows<T, R>(y + k0, acc, make_policy(MODE == STORE_DIRECT_DOT ? 0 : y_kind - 1));
@@ -349,8 +368,14 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
         y[k] = acc[r];
       } else {
         const int p = perm[k];
-        if (MODE == STORE_PERM_ACC) y[p] = y[p] + acc[r];
-        else y[p] = acc[r];
+        if (p_kind) {
+          const uint64_t pp = make_policy(p_kind - 1);
+          st_one(y + p, MODE == STORE_PERM_ACC ? ld_one(y + p, pp) + acc[r] : acc[r], pp);
+        } else if (MODE == STORE_PERM_ACC) {
+          y[p] = y[p] + acc[r];
+        } else {
+          y[p] = acc[r];
+        }
       }
     }
   }
@@ -638,8 +663,11 @@ int st;
     if (st != PJDS_OK) return st;
     if (done) return PJDS_OK;
   }
-  // the vector y store needs y aligned to R elements (caller pointers need only T alignment)
-  const int pol = ((uintptr_t)y % (R * sizeof(T))) ? (g_pol & 0xffff) : g_pol;
+  // per-handle y-store override (dist A_loc: its y is read again by the nonlocal pass), then the
+  // vector y store needs y aligned to R elements (caller pointers need only T alignment)
+  int pol = g_pol;
+  if (A->y_store >= 0) pol = (pol & 0xff00ffff) | ((A->y_store & 0xff) << 16);
+  if ((uintptr_t)y % (R * sizeof(T))) pol &= 0xff00ffff;
 #define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
   pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, pol, order, dot_part, h.sigma, \
@@ -874,12 +902,15 @@ int set_schedule(int mode) { return set_schedule_impl(mode); }
 
 int set_cache_policy(int stream_kind, int x_kind) {
   // bits 8-15 of stream_kind: y store of the permuted-basis kernel (0 plain scalar stores,
-  // 1 + kind: one R-wide vector store with that L2 policy; default 2 = vector, evict_first)
+  // 1 + kind: one R-wide vector store with that L2 policy; default 2 = vector, evict_first);
+  // bits 16-23: the scattered stores through perm (row-only basis, dist nonlocal +=): 0 plain
+  // (default), 1 + kind: L1::no_allocate store (and load for +=) with that L2 policy
   const int y_kind = (stream_kind >> 8) & 0xff;
+  const int p_kind = (stream_kind >> 16) & 0xff;
   stream_kind &= 0xff;
-  if (stream_kind > 3 || x_kind < 0 || x_kind > 3 || y_kind > 4)
+  if (stream_kind > 3 || x_kind < 0 || x_kind > 3 || y_kind > 4 || p_kind > 4)
     return set_error(PJDS_ERR_INVALID_ARG, "cache policy kinds: 0 normal, 1 evict_first, 2 evict_last, 3 unchanged");
-  g_pol = stream_kind | (x_kind << 8) | (y_kind << 16);
+  g_pol = stream_kind | (x_kind << 8) | (y_kind << 16) | (p_kind << 24);
   return PJDS_OK;
 }
 
