@@ -372,6 +372,12 @@ int pjds_dist_parts(pjds_dist_t D, pjds_t* A_loc, pjds_t* A_nl);
    region).  Collective in effect: synchronise all ranks' streams and barrier before destroying, so
    no peer still writes into (P2P) or exchanges with (NCCL) this rank. */
 int pjds_dist_destroy(pjds_dist_t D);
+/* Tuning knob (process-wide, read by later pjds_dist_create calls): sort scope of the nonlocal part
+   A_nl in rows.  Default 1024: the nonlocal rows are taken in ascending order of their y target
+   and sorted by length only within windows of 1024 rows (one CTA tile), so the y += of a CTA
+   touches one compact range of y; 0 = the global sort over all nonlocal rows.  Every row's chain
+   is the same either way (bitwise-identical y).  INVALID_ARG unless 0 or a multiple of 1024. */
+int pjds_set_dist_nl_sigma(int64_t sigma);
 
 /* NCCL helpers (NCCL is dlopen-ed; `libpath` NULL tries "libnccl.so.2"). */
 int pjds_nccl_load(const char* libpath);
@@ -448,7 +454,9 @@ int pjds_set_y_store(pjds_t A, int32_t kind);
 /* Tuning knob (process-wide): execution order of the pJDS kernel's CTA tiles.  0 = storage
    order (longest blocks first); 1 = tiles ordered by the original index of their first row, so
    rows of all length classes from one region of the matrix run together (RHS reuse in L2,
-   local y stores); 2 = auto (default): 1 in the row-only basis or when x exceeds 64 MB, else 0.
+   local y stores); 2 = auto (default): 1 in the row-only basis or when x exceeds 64 MB, else 0;
+   3 = the key of mode 1 at warp-tile granularity (32 R sorted rows): each warp of a CTA takes the
+   warp tile a table assigns, so one CTA mixes length classes of one region (sort scope 0 only).
    The per-row arithmetic, and therefore y, is identical. */
 int pjds_set_tile_order(int32_t mode);
 /* pjds_set_schedule (process-wide knob; results are identical): 0 = static grid of CTA tiles

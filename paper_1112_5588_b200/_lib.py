@@ -106,6 +106,7 @@ _SIGS = {
     "pjds_dist_parts": [c_p, c_p, c_p],
     "pjds_dist_destroy": [c_p],
     "pjds_nccl_load": [ctypes.c_char_p],
+    "pjds_set_dist_nl_sigma": [c_i64],
     "pjds_nccl_unique_id": [c_p],
     "pjds_bw_probe": [c_i64, c_i32, c_p, c_p],
     "pjds_set_kernel_variant": [c_i32, c_i32],

@@ -43,6 +43,10 @@ int free_pjds_device(pjds_mat* A) {
     cudaFree(o);
     o = nullptr;
   }
+  for (auto& o : A->d_worder) {
+    cudaFree(o);
+    o = nullptr;
+  }
   A->d_val = A->d_xs = A->d_ys = nullptr;
   A->d_col = A->d_block_len = A->d_perm = nullptr;
   A->d_col_start = nullptr;

@@ -46,6 +46,8 @@ struct pjds_plan {
 namespace {
 
 constexpr int kMaxRuns = 64;
+// sort scope of the nonlocal part A_nl (rows per window; 0 = the global sort), see dist create
+int64_t g_nl_sigma = 1024;
 
 // ---- NCCL (dlopen) ------------------------------------------------------------------------
 struct Nccl {
@@ -271,6 +273,13 @@ struct P2PBlob {
 extern "C" {
 
 int pjds_nccl_load(const char* libpath) { return nccl_load(libpath); }
+
+int pjds_set_dist_nl_sigma(int64_t sigma) {
+  if (sigma < 0 || (sigma > 0 && sigma % 1024 != 0))
+    return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_dist_nl_sigma: 0 or a multiple of 1024");
+  g_nl_sigma = sigma;
+  return PJDS_OK;
+}
 
 int pjds_nccl_unique_id(void* out128) {
   if (!out128) return set_error(PJDS_ERR_INVALID_ARG, "pjds_nccl_unique_id: NULL");
@@ -590,13 +599,32 @@ static int dist_create_impl(pjds_dist_t* out, pjds_plan_t P, const void* val, in
       const int64_t m = (int64_t)P->rows_nl.size();
       if (m > 0) {
         D->A_nl = new pjds_mat();
-        s = convert_pjds(D->A_nl->h, m, std::max<int64_t>(D->halo, 1), P->nl_rowptr.data(), P->nl_col.data(),
-                         v_nl.data(), dtype, block_rows, false);
-        // store to local row rows_nl[perm_nl[k]] (or its position in the local permuted basis)
+        // store target of each nonlocal row: its local row (or its position in the local permuted
+        // basis).  The nonlocal rows are taken in ascending TARGET order and sorted by length only
+        // inside windows of g_nl_sigma rows (one CTA tile each), so the y += of one CTA touches one
+        // compact range of y instead of scattered 8-byte read-modify-writes.  Each row's chain
+        // (its nonlocal entries in CRS order) is unchanged, so y is bitwise the same.
         std::vector<int32_t> map(P->rows_nl);
         if (sym)
           for (auto& r : map) r = inv[r];
-        if (s == PJDS_OK) s = upload_pjds(D->A_nl, map.data());
+        const int64_t nlsig = (g_nl_sigma > 0 && g_nl_sigma % 1024 == 0 && g_nl_sigma % block_rows == 0) ? g_nl_sigma : 0;
+        std::vector<int64_t> ord(m);
+        for (int64_t a = 0; a < m; ++a) ord[a] = a;
+        if (nlsig && sym)
+          std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return map[x] < map[y]; });
+        std::vector<int64_t> orp(m + 1, 0);
+        for (int64_t a = 0; a < m; ++a) orp[a + 1] = orp[a] + (P->nl_rowptr[ord[a] + 1] - P->nl_rowptr[ord[a]]);
+        std::vector<int32_t> ocol(orp[m]), omap(m);
+        std::vector<uint8_t> oval(orp[m] * vs);
+        for (int64_t a = 0; a < m; ++a) {
+          const int64_t r = ord[a], b0 = P->nl_rowptr[r], cnt = P->nl_rowptr[r + 1] - b0;
+          std::memcpy(&ocol[orp[a]], &P->nl_col[b0], cnt * 4);
+          std::memcpy(&oval[orp[a] * vs], &v_nl[b0 * vs], cnt * vs);
+          omap[a] = map[r];
+        }
+        s = convert_pjds(D->A_nl->h, m, std::max<int64_t>(D->halo, 1), orp.data(), ocol.data(), oval.data(), dtype,
+                         block_rows, false, nlsig);
+        if (s == PJDS_OK) s = upload_pjds(D->A_nl, omap.data());
         if (s != PJDS_OK) return fail(s);
         D->A_nl->ncols = D->halo;
       }

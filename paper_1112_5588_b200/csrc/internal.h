@@ -99,6 +99,7 @@ struct pjds_mat {
   int64_t ncols = 0;
   bool direct_store = false;  // permuted basis: y[k] stored contiguously, perm not read
   int32_t* d_order[3] = {nullptr, nullptr, nullptr};  // CTA tile execution orders (R = 1, 2, 4)
+  int32_t* d_worder[3] = {nullptr, nullptr, nullptr};  // warp-tile (32 R rows) execution orders
   // fused remote-gather dist matrix (PJDS_TRANSPORT_DIRECT): column codes (owner << win_shift) |
   // position; d_win = device table of 64 x-window base pointers (owned by the dist handle)
   void** d_win = nullptr;

@@ -324,18 +324,32 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
                  double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off,
-                 const T* const* __restrict__ win, int win_shift) {
+                 const T* const* __restrict__ win, int win_shift, const int* __restrict__ warp_order,
+                 int64_t n_wtiles) {
   __shared__ Off s_cs[kSmemCS];
   __shared__ const T* s_win[WIN ? kMaxWin : 1];
   if constexpr (WIN)
     for (int i = threadIdx.x; i < kMaxWin; i += kThreads) s_win[i] = win[i];
-  // execution order of the CTA tiles (storage order, or by original row; results are identical)
-  const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
-  const int64_t t = tile * kThreads + threadIdx.x;
   constexpr int RS = IL ? 32 : 1;  // distance between a thread's rows
-  const int64_t k0 = IL ? ((t & ~int64_t(31)) * R + (t & 31)) : t * R;
-  const int64_t cta_k0 = tile * kThreads * R;
-  const int cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
+  int64_t k0, cta_k0;
+  int cta_len;
+  if (!IL && warp_order) {
+    // warp-granular order (tile order mode 3): each warp takes the warp tile (32 R consecutive
+    // sorted rows) the table assigns to its slot, so one CTA runs warp tiles of several length
+    // classes from one region of the original matrix; staged col_start covers the widest (block 0)
+    const int64_t slot = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const int64_t wt = slot < n_wtiles ? (int64_t)warp_order[slot] : (n_pad / (32 * R) + 1);
+    k0 = wt * 32 * R + (int64_t)(threadIdx.x & 31) * R;
+    cta_k0 = 0;
+    cta_len = block_len[0];
+  } else {
+    // execution order of the CTA tiles (storage order, or by original row; results are identical)
+    const int64_t tile = tile_order ? (int64_t)tile_order[blockIdx.x] : (int64_t)blockIdx.x;
+    const int64_t t = tile * kThreads + threadIdx.x;
+    k0 = IL ? ((t & ~int64_t(31)) * R + (t & 31)) : t * R;
+    cta_k0 = tile * kThreads * R;
+    cta_len = block_len[cta_k0 / br];  // first block of the CTA is its longest
+  }
   // sort window of this CTA (CTAs never straddle windows: sigma is a multiple of the tile size);
   // its col_start table already includes the window's storage offset (kernel view)
   col_start += wcs_off[cta_k0 / sigma];
@@ -348,7 +362,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = T(0);
   if (active) {
-  const int64_t warp_k0 = (t & ~int64_t(31)) * R;
+  const int64_t warp_k0 = IL ? (k0 - (threadIdx.x & 31)) : (k0 - (int64_t)(threadIdx.x & 31) * R);
   const int wlen = block_len[warp_k0 / br];
   const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
   const uint64_t pol_s = make_policy(pol & 0xff);
@@ -551,7 +565,8 @@ pjds_spmv_split_kernel(const T* __restrict__ val, const int* __restrict__ col, c
 }
 
 static int g_pol = 1 | (2 << 8) | (2 << 16);  // val/col evict_first, x evict_last, y vector store evict_first
-static int g_tile_order = 2;  // 0 storage order, 1 by first row's original index, 2 auto (see launch_pjds_t)
+static int g_tile_order = 2;  // 0 storage order, 1 by first row's original index, 2 auto (see launch_pjds_t),
+                              // 3 warp tiles by their first row's original index
 
 // Tiles (CTAs of rows_per_tile consecutive sorted rows) ordered by the original index of their first
 // row: all length classes of one region of the original matrix run together, so the RHS entries
@@ -563,7 +578,8 @@ int tile_order_for(const pjds_mat* A, int R, const int** out) {
 }
 
 int set_tile_order_impl(int mode) {
-  if (mode < 0 || mode > 2) return set_error(PJDS_ERR_INVALID_ARG, "tile order: 0 storage, 1 original-row, 2 auto");
+  if (mode < 0 || mode > 3)
+    return set_error(PJDS_ERR_INVALID_ARG, "tile order: 0 storage, 1 original-row, 2 auto, 3 warp-granular original-row");
   g_tile_order = mode;
   return PJDS_OK;
 }
@@ -653,8 +669,11 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
                       (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
                        (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(A, R, &order));
+  const bool by_warp = g_tile_order == 3 && h.n_windows <= 1 && !(g_il && R > 1) && !A->d_win;
+  const int* worder = by_warp ? A->d_worder[R == 4 ? 2 : (R == 2 ? 1 : 0)] : nullptr;
+  const int64_t n_wtiles = (h.n_pad + 32 * R - 1) / (32 * R);
   // grids of a few waves: dynamic warp tiles (same row chains, bitwise the same y)
-  if (A->d_sched && h.n_windows <= 1 && !(g_il && R > 1) && mode != STORE_DIRECT_DOT) {
+  if (A->d_sched && h.n_windows <= 1 && !(g_il && R > 1) && mode != STORE_DIRECT_DOT && !by_warp) {
     bool done = false;
 int st;
     if (mode == STORE_DIRECT) st = launch_dyn_any<T, Off, R, U, STORE_DIRECT>(A, y, x, s, order, grid, pipe, &done);
@@ -671,7 +690,7 @@ int st;
 #define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
   pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, pol, order, dot_part, h.sigma, \
-      A->d_wcs_off, (const T* const*)A->d_win, A->win_shift)
+      A->d_wcs_off, (const T* const*)A->d_win, A->win_shift, worder, n_wtiles)
 #define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
   if (A->d_win) {  // fused remote-gather dist matrix: plain main loop, direct or perm store
     if constexpr (std::is_same<Off, int32_t>::value) {
@@ -881,6 +900,19 @@ int build_tile_orders(pjds_mat* A, const int64_t* row_key) {
     std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
     if (!A->d_order[slot]) PJDS_CUDA_TRY(cudaMalloc(&A->d_order[slot], tiles * 4));
     PJDS_CUDA_TRY(cudaMemcpy(A->d_order[slot], ord.data(), tiles * 4, cudaMemcpyHostToDevice));
+    // the same key at warp-tile granularity (32 R rows)
+    const int64_t wrows = 32 * Rs[slot];
+    const int64_t wt = std::max<int64_t>((h.n_pad + wrows - 1) / wrows, 1);
+    std::vector<int64_t> wkey(wt);
+    for (int64_t t = 0; t < wt; ++t) {
+      const int64_t k = t * wrows;
+      wkey[t] = k < h.n ? (row_key ? row_key[h.perm[k]] : (int64_t)h.perm[k]) : INT64_MAX;
+    }
+    std::vector<int32_t> word(wt);
+    for (int64_t t = 0; t < wt; ++t) word[t] = (int32_t)t;
+    std::stable_sort(word.begin(), word.end(), [&](int32_t a, int32_t b) { return wkey[a] < wkey[b]; });
+    if (!A->d_worder[slot]) PJDS_CUDA_TRY(cudaMalloc(&A->d_worder[slot], wt * 4));
+    PJDS_CUDA_TRY(cudaMemcpy(A->d_worder[slot], word.data(), wt * 4, cudaMemcpyHostToDevice));
   }
   return PJDS_OK;
 }

@@ -445,9 +445,9 @@ def test_permute_and_symmetric_host_e2e(pj):
     check_y(y, n, rp, col, val, x)
 
 
-@pytest.mark.parametrize("order", [0, 1, 2])
+@pytest.mark.parametrize("order", [0, 1, 2, 3])
 def test_tile_order_bitwise(pj, order):
-    """CTA execution order does not change any row's chain."""
+    """CTA (or, mode 3, warp-tile) execution order does not change any row's chain."""
     L = pj.lib()
     try:
         assert L.pjds_set_tile_order(order) == 0
@@ -460,6 +460,38 @@ def test_tile_order_bitwise(pj, order):
                 A.spmv_host(y, x)
                 check_y(y, n, rp, col, val, x)
     finally:
+        L.pjds_set_tile_order(2)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_warp_tile_order_variants_bitwise(pj, dtype):
+    """Mode 3 (warp tiles by original row) with every rows-per-thread variant, b_r 32/128, ragged
+    and empty-row inputs, both bases, the Lanczos-style fused dot kernel excluded (sigma = 0 only)."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_tile_order(3) == 0
+        cases = [("C3", None), ("random", 2500), ("empty_rows", 777), ("adversarial", 1100)]
+        for name, m in cases:
+            if m is None:
+                n, rp, col, val = inputs.config_crs(name, dtype=dtype)
+            else:
+                n, rp, col, val = inputs.small(name, m, seed=m, dtype=dtype, **({"max": 70} if name == "random" else {}))
+            x = inputs.vector(n, dtype)
+            xt = tdev(x)
+            for br in (32, 128):
+                for sym in (False, True):
+                    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, symmetric=sym)
+                    xin = A.to_permuted(torch.empty_like(xt), xt) if sym else xt
+                    for variant in ((0, 0), (1, 8), (2, 4), (4, 2), (4, 4)):
+                        assert L.pjds_set_kernel_variant(*variant) == 0
+                        y = torch.full_like(xt, float("nan"))
+                        A.spmv(y, xin)
+                        yo = A.from_permuted(torch.empty_like(y), y) if sym else y
+                        torch.cuda.synchronize()
+                        check_y(yo.cpu().numpy(), n, rp, col, val, x)
+                    del A
+    finally:
+        L.pjds_set_kernel_variant(0, 0)
         L.pjds_set_tile_order(2)
 
 

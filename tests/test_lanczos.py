@@ -88,13 +88,19 @@ def test_gpu_lanczos_matches_oracle(dtype):
         a, b, steps = A.lanczos(torch.from_numpy(v0[perm].copy()).cuda(), m)
         assert steps == m
         ra, rb = olz.lanczos(n, rp, col, val.astype(np.float64), v0.astype(np.float64), m)
-        tol = 1e-10 if dtype == np.float64 else 2e-4
+        # every coefficient of the m = 40 steps, not only the first ones: the GPU products are
+        # bitwise the oracle's FMA chains, so the recurrences differ only by the rounding of the
+        # dot products / vector updates.  Measured on B200 (tools/lanczos_drift.py,
+        # profiles/r02_lanczos_drift.jsonl): max |da|, |db| / scale = 6.2e-16 (DP), 6.6e-8 (SP)
+        # over all 40 steps; the bounds below leave ~100x (DP) / ~30x (SP) of headroom and are still
+        # 1e3-1e4 x tighter than a single wrong term or a dropped step would produce.
+        tol = 1e-13 if dtype == np.float64 else 2e-6
         scale = max(np.abs(ra).max(), np.abs(rb).max())
-        # early coefficients agree tightly; later ones drift with rounding (no re-orthogonalisation)
-        assert np.abs(a[:10] - ra[:10]).max() <= tol * scale, name
-        assert np.abs(b[:10] - rb[:10]).max() <= tol * scale, name
+        assert np.abs(a - ra).max() <= tol * scale, name
+        assert np.abs(b - rb).max() <= tol * scale, name
+        assert (b > 0).all(), name  # no breakdown on these matrices
         ev, rv = pj.tridiag_eigenvalues(a, b), olz.ritz_values(ra, rb)
-        assert abs(ev[0] - rv[0]) <= 10 * tol * scale and abs(ev[-1] - rv[-1]) <= 10 * tol * scale, name
+        assert np.abs(ev - rv).max() <= 10 * tol * scale, name  # all 40 Ritz values
 
 
 @pytest.mark.gpu

@@ -36,6 +36,7 @@ p.add_argument("--ystore", default="-1", help="comma list of A_loc y-store overr
 p.add_argument("--pstore", default="0", help="comma list of perm-store kinds for A_nl (0 plain, 1+kind)")
 p.add_argument("--all-ranks", action="store_true", help="emulate every rank (default: ranks 0 and R/2)")
 p.add_argument("--reps", type=int, default=20)
+p.add_argument("--nl-sigma", default="1024", help="comma list of A_nl sort scopes (pjds_set_dist_nl_sigma)")
 a = p.parse_args()
 SEG = {"C1": 1024, "C3": 15504, "C5": 142506}[a.config]
 npdt = np.float64 if a.dtype == "f64" else np.float32
@@ -73,11 +74,13 @@ for mode in a.modes.split(","):
     del A1, x1, y1
     torch.cuda.empty_cache()
 
-for mode in a.modes.split(","):
-    for R in map(int, a.ranks.split(",")):
+for mode, R, nls in [(m_, r_, s_) for m_ in a.modes.split(",") for r_ in map(int, a.ranks.split(","))
+                     for s_ in map(int, a.nl_sigma.split(","))]:
+    if True:
         nb = n // SEG
         offs = np.array([(nb * r // R) * SEG for r in range(R + 1)], np.int64)
         offs[-1] = n
+        assert pj.lib().pjds_set_dist_nl_sigma(nls) == 0
         hs = pj.DistPjds.create_group(n, rp, col, val, offs, permuted=(mode == "permuted"))
         which = range(R) if a.all_ranks else sorted({0, R // 2})
         for ys in map(int, a.ystore.split(",")):
@@ -129,6 +132,7 @@ for mode in a.modes.split(","):
                     del src, dst, x, y, halo, packbuf
                 tmax = max(rr["t_rank_us"] for rr in ranks)
                 print(json.dumps({"config": a.config, "dtype": a.dtype, "mode": mode, "R": R, "ystore": ys, "pstore": ps,
+                                  "nl_sigma": nls,
                                   "t1_us": round(t_single[mode] * 1e6, 1), "t_rank_max_us": round(tmax, 1),
                                   "efficiency_vs_t1": round(t_single[mode] * 1e6 / (R * tmax), 4),
                                   "ranks": [{k: (round(v, 1) if isinstance(v, float) else v) for k, v in rr.items()}

@@ -112,7 +112,8 @@ int main(int argc, char** argv) {
   std::vector<int32_t> perm(n), inv(n);
   for (int64_t i = 0; i < n; ++i) perm[cnt[maxlen - len[i]]++] = (int32_t)i;
   for (int64_t k = 0; k < n; ++k) inv[perm[k]] = (int32_t)k;
-  const int64_t TR = 1024, ntiles = (n + TR - 1) / TR;
+  const int64_t TR = getenv("L2SIM_TILE") ? atoll(getenv("L2SIM_TILE")) : 1024, ntiles = (n + TR - 1) / TR;
+  const int64_t GROUP = getenv("L2SIM_GROUP") ? atoll(getenv("L2SIM_GROUP")) : 1;  // tiles per L1 dedup unit
   // P (rows per e-block) from the generator's structure: the HMEp phonon count C(M+5,5)
   int64_t P = 1;
   for (int k = 1; k <= 5; ++k) P = P * (M + k) / k;
@@ -146,20 +147,26 @@ int main(int argc, char** argv) {
     for (int64_t cap : caps) {
       Cache c(cap);
       std::vector<int64_t> secs;
-      for (int64_t oi = 0; oi < ntiles; ++oi) {
-        const int64_t t = order[oi];
+      int64_t l1_sectors = 0;
+      for (int64_t oi0 = 0; oi0 < ntiles; oi0 += GROUP) {
         secs.clear();
-        for (int64_t k = t * TR; k < std::min(n, (t + 1) * TR); ++k) {
-          const int32_t r = perm[k];
-          for (int64_t q = rp[r]; q < rp[r + 1]; ++q) secs.push_back(((int64_t)inv[col[q]] * 8) >> 5);
+        for (int64_t oi = oi0; oi < std::min(ntiles, oi0 + GROUP); ++oi) {
+          const int64_t t = order[oi];
+          for (int64_t k = t * TR; k < std::min(n, (t + 1) * TR); ++k) {
+            const int32_t r = perm[k];
+            for (int64_t q = rp[r]; q < rp[r + 1]; ++q) secs.push_back(((int64_t)inv[col[q]] * 8) >> 5);
+          }
         }
         std::sort(secs.begin(), secs.end());
         secs.erase(std::unique(secs.begin(), secs.end()), secs.end());
+        l1_sectors += (int64_t)secs.size();
         for (int64_t s : secs) c.access(s);
       }
       const double xbytes = c.misses * 32.0;
-      printf("{\"spec\": \"%s\", \"cap_mb\": %ld, \"x_dram_gb\": %.4f, \"alpha\": %.4f, \"loads_per_x\": %.3f}\n",
-             spec.c_str(), (long)(cap >> 20), xbytes / 1e9, xbytes / (nnz * 8.0), xbytes / (n * 8.0));
+      printf("{\"spec\": \"%s\", \"tile\": %ld, \"group\": %ld, \"cap_mb\": %ld, \"x_dram_gb\": %.4f, \"alpha\": %.4f, "
+             "\"loads_per_x\": %.3f, \"l2_x_requests_gb\": %.3f}\n",
+             spec.c_str(), (long)TR, (long)GROUP, (long)(cap >> 20), xbytes / 1e9, xbytes / (nnz * 8.0),
+             xbytes / (n * 8.0), l1_sectors * 32.0 / 1e9);
       fflush(stdout);
     }
   }
