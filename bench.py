@@ -12,7 +12,8 @@ At N=1 the product runs in the permuted basis (PJDS_PERM_SYMMETRIC), the paper's
 iterative solvers: "permutation of the indices needs to be done only before the start and after
 the end of the algorithm, while the complete iterative scheme works on the permuted elements"
 (PAPER.md L241-246); x is permuted once before the timed region (--basis rows: y stored through
-perm every step instead).  Beside the headline the N=1 line carries:
+perm every step instead).  At N>1 the NCCL / P2P split runs in the original basis by default (its
+halo lists are then contiguous runs of x: no pack kernel), DIRECT in the permuted basis.  Beside the headline the N=1 line carries:
   compare     rows-only pJDS, b_r = 128, ELLPACK-R and cuSPARSE CSR on the same matrix;
   per_config  the SURVEY §8(d) targets table: C2/C3 DP+SP, C4 DP+SP, C5 SP, each pJDS and
               ELLPACK-R timed with L2 carry-over of x defeated (x/y rotated over sets larger than
@@ -77,7 +78,10 @@ def parse(argv=None):
     p.add_argument("--impl", default="pjds", choices=["pjds", "ellr", "reference"])
     p.add_argument("--config", default="C5", choices=sorted(CONFIG_DESC))
     p.add_argument("--dtype", default="f64", choices=["f64", "f32"])
-    p.add_argument("--basis", default="permuted", choices=["permuted", "rows"])
+    p.add_argument("--basis", default="auto", choices=["auto", "permuted", "rows"],
+                   help="auto: the permuted basis at N=1 and for the DIRECT transport; the original basis "
+                        "(rows permuted, y stored through perm) for the NCCL / P2P split, whose halo lists "
+                        "then are contiguous runs of x (no pack)")
     p.add_argument("--block-rows", type=int, default=32, help="pJDS b_r (the paper's warp size; 128 = rows per warp at R=4)")
     p.add_argument("--no-overlap", action="store_true", help="dist: vector mode (exchange, then compute)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -423,7 +427,7 @@ def run_single(a, npdt, sv, argv_cfg):
     rp, col, val = g.crs(dtype=npdt)
     nnz = int(rp[-1])
     x_host = inputs.vector(n, npdt)
-    permuted = a.impl == "pjds" and a.basis == "permuted"
+    permuted = a.impl == "pjds" and a.basis in ("permuted", "auto")
     if a.impl == "ellr":
         A = pj.EllrMatrix.from_crs(n, rp, col, val)
     else:
@@ -488,7 +492,7 @@ def run_single(a, npdt, sv, argv_cfg):
     # algorithmic bytes (Eq. 1 at alpha = 1/N_nzr, write-only y): val+col once, x once, y once
     b_min = nnz * (sv + 4) + 2 * n * sv
     achieved = b_min / t_s / 1e9
-    traffic_key = (f"{a.config}/{a.dtype}/{a.basis if a.impl == 'pjds' else 'ellr'}"
+    traffic_key = (f"{a.config}/{a.dtype}/{('permuted' if permuted else 'rows') if a.impl == 'pjds' else 'ellr'}"
                    + ("" if a.block_rows == 32 else f"/br{a.block_rows}")
                    + (f"/tw{a.tile_window}" if a.tile_window else ""))
     traffic, traffic_src = committed_traffic(traffic_key)
@@ -705,13 +709,16 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     rp, col, val = g.crs(lo, hi, dtype=npdt)
     nnz_loc = int(rp[-1])
     x_host = inputs.vector(hi - lo, npdt, i0=lo)
-    permuted = a.basis == "permuted"
+    def basis_of(transport):
+        return a.basis == "permuted" or (a.basis == "auto" and transport == "direct")
+
+    permuted = basis_of(a.transport)
 
     def build(transport):
-        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=permuted,
+        D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=basis_of(transport),
                                transport=transport)
         xd = torch.from_numpy(x_host).to(dev)
-        if permuted:
+        if basis_of(transport):
             xd = D.to_permuted(torch.empty_like(xd), xd)
         if transport == "direct":  # x lives in the exported window: no per-call copy
             w = D.x_window()
@@ -765,8 +772,8 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
         x_full = inputs.vector(n, npdt)
         ref = oracle_rows(g, chunks, x_full, npdt)
 
-    def parity_of(Dh, yv, chain_expected):
-        yo = Dh.from_permuted(torch.empty_like(yv), yv, stream=stream) if permuted else yv
+    def parity_of(Dh, yv, chain_expected, perm_basis):
+        yo = Dh.from_permuted(torch.empty_like(yv), yv, stream=stream) if perm_basis else yv
         torch.cuda.synchronize()
         finite = torch.tensor([int(bool(torch.isfinite(yo).all().item()))], dtype=torch.int64, device=dev)
         _allreduce(dist, finite, "sum")
@@ -786,7 +793,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     to_main = timed_out(D)
     # NCCL / P2P split the row into local + nonlocal chains (combined by one add, DESIGN reading 25):
     # not the unsplit O3 chain; DIRECT runs every row's whole chain in one kernel (bitwise expected)
-    parity = parity_of(D, y, chain_expected=a.transport == "direct")
+    parity = parity_of(D, y, chain_expected=a.transport == "direct", perm_basis=permuted)
     if parity is not None:
         parity["peer_wait_timed_out"] = to_main
         if to_main:
@@ -833,9 +840,9 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
                 dist.barrier()
                 m2 = max_over_ranks(dist, dev, timed(lambda i: D2.spmv(y2, x2, stream=stream), max(10, a.steps // 2)))
                 to2 = timed_out(D2)
-                p2 = parity_of(D2, y2, chain_expected=trn == "direct")
+                p2 = parity_of(D2, y2, chain_expected=trn == "direct", perm_basis=basis_of(trn))
                 leg = {"ms": round(m2, 5), "GFlop/s": round(2.0 * nnz / (m2 * 1e-3) / 1e9, 1),
-                       "peer_wait_timed_out": to2}
+                       "peer_wait_timed_out": to2, "basis": "permuted" if basis_of(trn) else "rows"}
                 if p2 is not None:
                     leg["parity_within_bound"] = p2["within_bound"] and not to2
                     leg["parity_bitwise_o3_chain"] = p2["bitwise_o3_chain"]
@@ -853,10 +860,13 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     if not a.no_t1 and world > 1:
         if rank == 0:
             rp1, col1, val1 = g.crs(dtype=npdt)
-            A1 = pj.PjdsMatrix.from_crs(n, rp1, col1, val1, block_rows=a.block_rows, symmetric=permuted)
+            # the N=1 bench's configuration (permuted basis unless --basis rows): the same T_1 the
+            # driver divides by when it computes efficiency from the per-N lines
+            p1 = a.basis != "rows"
+            A1 = pj.PjdsMatrix.from_crs(n, rp1, col1, val1, block_rows=a.block_rows, symmetric=p1)
             del rp1, col1, val1
             x1 = torch.from_numpy(x_full).to(dev)
-            if permuted:
+            if p1:
                 x1 = A1.to_permuted(torch.empty_like(x1), x1)
             y1 = torch.empty(n, dtype=tdt, device=dev)
             for _ in range(5):

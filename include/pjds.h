@@ -454,9 +454,10 @@ int pjds_set_y_store(pjds_t A, int32_t kind);
 /* Tuning knob (process-wide): execution order of the pJDS kernel's CTA tiles.  0 = storage
    order (longest blocks first); 1 = tiles ordered by the original index of their first row, so
    rows of all length classes from one region of the matrix run together (RHS reuse in L2,
-   local y stores); 2 = auto (default): 1 in the row-only basis or when x exceeds 64 MB, else 0;
-   3 = the key of mode 1 at warp-tile granularity (32 R sorted rows): each warp of a CTA takes the
-   warp tile a table assigns, so one CTA mixes length classes of one region (sort scope 0 only).
+   local y stores); 3 = the key of mode 1 at warp-tile granularity (32 R sorted rows): each warp of
+   a CTA takes the warp tile a table assigns, so one CTA mixes length classes of one region (sort
+   scope 0 only); 2 = auto (default): 3 for the row-only basis when no length class holds 90 % of
+   the rows, else 1 in the row-only basis or when x exceeds 64 MB, else 0.
    The per-row arithmetic, and therefore y, is identical. */
 int pjds_set_tile_order(int32_t mode);
 /* pjds_set_schedule (process-wide knob; results are identical): 0 = static grid of CTA tiles

@@ -89,6 +89,11 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
     free_pjds_device(A);
     return s;
   }
+  {
+    int64_t mx = 0;
+    for (int64_t c : h.hist) mx = std::max(mx, c);
+    A->mixed_classes = h.n > 0 && (double)mx < 0.9 * (double)h.n;
+  }
   if ((s = build_tile_orders(A)) != PJDS_OK) {
     free_pjds_device(A);
     return s;

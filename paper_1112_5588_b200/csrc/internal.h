@@ -109,6 +109,9 @@ struct pjds_mat {
   // 0 plain stores or 1 + L2 policy kind of the vector store), e.g. a dist A_loc whose y the
   // nonlocal pass reads again
   int32_t y_store = -1;
+  // no length class holds >= 90 % of the rows (set at upload): the auto tile order then runs the
+  // row-only kernels in warp-granular original-row order (mode 3)
+  bool mixed_classes = false;
 };
 
 struct ellr_mat {

@@ -669,7 +669,12 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
                       (g_tile_order == 2 && h.n_windows <= 1 &&  // windowed sorts already run in row order
                        (mode == STORE_PERM || mode == STORE_PERM_ACC || A->ncols * (int64_t)sizeof(T) > (int64_t(64) << 20)));
   if (by_row) PJDS_TRY(tile_order_for(A, R, &order));
-  const bool by_warp = g_tile_order == 3 && h.n_windows <= 1 && !(g_il && R > 1) && !A->d_win;
+  // warp-granular order (mode 3; auto: the row-only / accumulate stores when no length class
+  // dominates -- measured C5 DP rows-only 2384 -> 2256 us, C3 253 -> 238, C4 84 -> 81; the sAMG C2,
+  // 96 % of rows in one class, loses 16 % with it, and the permuted basis loses 1-3 %)
+  const bool by_warp = (g_tile_order == 3 || (g_tile_order == 2 && A->mixed_classes &&
+                                              (mode == STORE_PERM || mode == STORE_PERM_ACC))) &&
+                       h.n_windows <= 1 && !(g_il && R > 1) && !A->d_win;
   const int* worder = by_warp ? A->d_worder[R == 4 ? 2 : (R == 2 ? 1 : 0)] : nullptr;
   const int64_t n_wtiles = (h.n_pad + 32 * R - 1) / (32 * R);
   // grids of a few waves: dynamic warp tiles (same row chains, bitwise the same y)
