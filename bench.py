@@ -99,6 +99,9 @@ def parse(argv=None):
     p.add_argument("--transport", default="nccl", choices=["nccl", "p2p", "direct"],
                    help="dist: NCCL send/recv on a side stream, the fused gather+put P2P kernel, or DIRECT "
                         "(no exchange: one kernel whose nonlocal gathers read the owners' x windows)")
+    p.add_argument("--nccl-env", action="append", default=[], metavar="KEY=VALUE",
+                   help="NCCL tuning variable set before the communicator is created and recorded in the line "
+                        "(e.g. NCCL_P2P_USE_CUDA_MEMCPY=1, NCCL_MAX_CTAS=4, NCCL_MAX_P2P_NCHANNELS=8); repeatable")
     p.add_argument("--oversubscribe", action="store_true",
                    help="allow more ranks than visible GPUs (test mode: gloo group, one-GPU NCCL stand-in)")
     return p.parse_args(argv)
@@ -683,6 +686,13 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     import inputs
     import paper_1112_5588_b200 as pj
 
+    nccl_env = {}
+    for kv in a.nccl_env:  # must precede the first communicator (torch's and the library's)
+        k, _, v = kv.partition("=")
+        if not k.startswith("NCCL_") or not v:
+            raise SystemExit(f"bench.py: --nccl-env needs NCCL_*=value, got {kv!r}")
+        os.environ[k] = v
+        nccl_env[k] = v
     ngpu = torch.cuda.device_count()
     oversub = world > ngpu
     dev_index = local_rank % max(ngpu, 1)  # more ranks than GPUs only in --oversubscribe test mode
@@ -822,7 +832,8 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
                  "hidden_fraction": round(1.0 - max(0.0, tp["total"] - tp["local"] - tp["nonlocal"] - tp["pack"]) / comm, 3),
                  "halo_entries_rank0": D.info["halo"], "nnz_nonlocal_rank0": D.info["nnz_nonlocal_part"],
                  "messages_rank0": D.info["send_messages"], "row_offsets": offs.tolist(),
-                 "oversubscribed": oversub}
+                 "oversubscribed": oversub, "nccl_env": nccl_env or None,
+                 "basis": "permuted" if permuted else "rows"}
 
     # the other transports on the same partition, behind their bounded waits (compare legs)
     legs = {}
