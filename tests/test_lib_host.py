@@ -223,3 +223,39 @@ def test_dist_plan_hmep_segments(pj):
         assert all(c % 1024 == 0 for c in counts)
         runs = 1 + int(np.count_nonzero(np.diff(cols) != 1)) if len(cols) else 0
         assert runs == len(cols) // 1024 or runs < len(cols) // 1024  # adjacent segments merge
+
+
+def test_round2_knobs_and_collective_create_validation(pj):
+    """Argument checks of the round-2 entry points that need no GPU: the A_nl sort scope, the
+    per-handle y store, pjds_spmv_accum on host-only / symmetric handles, and the one-call
+    collective create's validation before any NCCL call (NULL id with nranks > 1, bad offsets)."""
+    L = pj.lib()
+    assert L.pjds_set_dist_nl_sigma(1000) == -1 and L.pjds_set_dist_nl_sigma(-1024) == -1
+    assert L.pjds_set_dist_nl_sigma(0) == 0 and L.pjds_set_dist_nl_sigma(2048) == 0
+    assert L.pjds_set_dist_nl_sigma(1024) == 0  # back to the default
+    assert L.pjds_set_schedule(4) == -1 and L.pjds_set_schedule(3) == 0
+    assert L.pjds_set_tile_order(4) == -1 and L.pjds_set_tile_order(2) == 0
+    n = 64
+    _, rp, col, val = inputs.small("random", n, seed=2, max=9)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, host_only=True)
+    assert L.pjds_set_y_store(A._h, 5) == -1 and L.pjds_set_y_store(A._h, -2) == -1
+    assert L.pjds_set_y_store(A._h, 3) == 0 and L.pjds_set_y_store(A._h, -1) == 0
+    assert L.pjds_set_y_store(None, 0) == -1
+    assert L.pjds_spmv_accum(A._h, ctypes.c_void_p(16), ctypes.c_void_p(32), None) == -1  # host-only
+    S = pj.PjdsMatrix.from_crs(n, rp, col, val, host_only=True, symmetric=True)
+    assert S.symmetric and not A.symmetric
+    h = ctypes.c_void_p()
+    offs = np.array([0, 32, 64], np.int64)
+    lo_rp = rp[:33] - rp[0]
+    # nranks > 1 needs the NCCL unique id
+    st = L.pjds_dist_create_crs(ctypes.byref(h), None, 2, 0, n, offs.ctypes.data, lo_rp.ctypes.data,
+                                col.ctypes.data, val.ctypes.data, 1, 32, 0)
+    assert st == -1 and not h.value
+    # offsets that do not span [0, n]
+    bad = np.array([0, 32, 60], np.int64)
+    uid = (ctypes.c_char * 128)()
+    st = L.pjds_dist_create_crs(ctypes.byref(h), uid, 2, 0, n, bad.ctypes.data, lo_rp.ctypes.data,
+                                col.ctypes.data, val.ctypes.data, 1, 32, 0)
+    assert st == -1 and not h.value
+    assert L.pjds_dist_create_crs(None, uid, 1, 0, n, offs.ctypes.data, rp.ctypes.data, col.ctypes.data,
+                                  val.ctypes.data, 1, 32, 0) == -1
