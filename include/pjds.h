@@ -460,17 +460,12 @@ int pjds_set_y_store(pjds_t A, int32_t kind);
    the rows, else 1 in the row-only basis or when x exceeds 64 MB, else 0.
    The per-row arithmetic, and therefore y, is identical. */
 int pjds_set_tile_order(int32_t mode);
-/* pjds_set_schedule (process-wide knob; results are identical): 0 = static grid of CTA tiles;
-   1 = dynamic warp tiles (a persistent grid of SMs x resident CTAs whose warps take tiles of 32R
-   sorted rows from a per-handle counter; measured slower on every config -- the scattered warp
-   tiles lose the L1 reuse of x between adjacent rows; kept as an experiment; a handle must not run
-   on two streams at once under it); 2 = work-balanced persistent grid (SMs x resident CTAs, CTA b
-   runs the contiguous warp-tile range [bal[b], bal[b+1]) cut at equal rows x length: no wave
-   quantisation, no CTA of longest rows finishing alone; the table is built on the host at the
-   first launch of a handle, so capture a CUDA graph only after one eager launch); 3 = auto
-   (default): 2 when the static grid would be fewer than 8 waves, else 0.  Not used by the
-   Lanczos-fused product, sigma-windowed handles, DIRECT window matrices or the lane-interleaved
-   variant. */
+/* pjds_set_schedule (process-wide knob; results are identical): 0 = static grid of CTA tiles
+   (default); 1 = dynamic warp tiles (a persistent grid of SMs x resident CTAs whose warps take
+   tiles of 32R sorted rows from a per-handle counter).  Measured slower on every config (the
+   scattered warp tiles lose the L1 reuse of x between adjacent rows); kept as an experiment.  A
+   handle must not run on two streams at once under the dynamic schedule.  Not used by the
+   Lanczos-fused product, sigma-windowed handles or the lane-interleaved variant. */
 int pjds_set_schedule(int32_t mode);
 
 /* Number of kernel launches this library has enqueued (process-wide counter). */

@@ -47,11 +47,6 @@ int free_pjds_device(pjds_mat* A) {
     cudaFree(o);
     o = nullptr;
   }
-  for (int k = 0; k < 3; ++k) {
-    cudaFree(A->d_bal[k]);
-    A->d_bal[k] = nullptr;
-    A->bal_grid[k] = 0;
-  }
   A->d_val = A->d_xs = A->d_ys = nullptr;
   A->d_col = A->d_block_len = A->d_perm = nullptr;
   A->d_col_start = nullptr;

@@ -112,10 +112,6 @@ struct pjds_mat {
   // no length class holds >= 90 % of the rows (set at upload): the auto tile order then runs the
   // row-only kernels in warp-granular original-row order (mode 3)
   bool mixed_classes = false;
-  // balanced persistent schedule: per rows-per-thread slot, the warp-tile range start of every CTA
-  // of a grid of bal_grid CTAs (built at first use for that grid size)
-  int64_t* d_bal[3] = {nullptr, nullptr, nullptr};
-  int32_t bal_grid[3] = {0, 0, 0};
 };
 
 struct ellr_mat {

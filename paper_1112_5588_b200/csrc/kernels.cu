@@ -406,71 +406,6 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   }
 }
 
-// Work-balanced persistent grid (schedule 2; automatic for grids of few waves).  A grid of
-// (SMs x resident CTAs) CTAs; CTA b owns the CONTIGUOUS range of warp tiles [bal[b], bal[b+1]) that
-// the host cut at equal work (rows x block length), and its warps take the range's tiles round
-// robin.  The static grid of a one- or few-wave matrix leaves SMs idle twice over: wave
-// quantisation (DLR1 SP: 544 CTAs over 740 slots, 100 SMs run 4 CTAs and 48 run 3) and the
-// longest rows' CTAs finishing last; equal work per CTA removes both, while adjacent tiles stay on
-// one SM (the L1 reuse the dynamic schedule lost).  Same row chains, bitwise the same y.
-// resident CTAs per SM the balanced kernel must keep (= those of the static kernel of the same
-// variant: its persistent loop would otherwise take 16-30 registers more than the static kernel)
-template <int R, int U, bool PIPE>
-constexpr int bal_min_blocks() { return (U >= 8 || (R == 4 && U == 4)) ? 2 : 4; }
-
-template <typename T, typename Off, int R, int U, int MODE, bool PIPE>
-__global__ void __launch_bounds__(kThreads, bal_min_blocks<R, U, PIPE>())
-pjds_spmv_bal_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
-                     const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
-                     T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int64_t* __restrict__ bal,
-                     int width) {
-  __shared__ Off s_cs[kSmemCS];
-  const int lim = min(width + 1, kSmemCS);  // every warp tile of the range may come here
-  for (int j = threadIdx.x; j < lim; j += kThreads) s_cs[j] = (Off)col_start[j];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t pol_s = make_policy(pol & 0xff);
-  const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
-  const int y_kind = (pol >> 16) & 0xff;
-  const int p_kind = (pol >> 24) & 0x7f;
-  const int t1 = (int)bal[blockIdx.x + 1];
-#pragma unroll 1
-  for (int wt = (int)bal[blockIdx.x] + warp; wt < t1; wt += kThreads / 32) {
-    const int64_t warp_k0 = (int64_t)wt * (32 * R);
-    const int64_t k0 = warp_k0 + lane * R;
-    if (k0 >= n_pad) continue;
-    const int wlen = block_len[warp_k0 / br];
-    const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
-    T acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = T(0);
-    row_chains<T, Off, R, U, PIPE, false, false>(acc, val, col, s_cs, col_start, k0, len, x, nullptr, 0, pol_s, pol_x);
-    if (MODE == STORE_DIRECT && R > 1 && y_kind && k0 + R <= n) {
-      st_rows<T, R>(y + k0, acc, make_policy(y_kind - 1));
-      continue;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t k = k0 + r;
-      if (k < n) {
-        if (MODE == STORE_DIRECT) {
-          y[k] = acc[r];
-        } else {
-          const int p = perm[k];
-          if (p_kind) {
-            const uint64_t pp = make_policy(p_kind - 1);
-            st_one(y + p, MODE == STORE_PERM_ACC ? ld_one(y + p, pp) + acc[r] : acc[r], pp);
-          } else if (MODE == STORE_PERM_ACC) {
-            y[p] = y[p] + acc[r];
-          } else {
-            y[p] = acc[r];
-          }
-        }
-      }
-    }
-  }
-}
-
 // Dynamic warp-tile schedule (opt-in experiment, pjds_set_schedule(1); measured slower, see g_sched).  A static grid of CTA
 // tiles leaves SMs idle in the last partial wave, and with one wave (DLR1: 544 CTAs) the SMs that
 // drew the longest rows finish last.  Here a persistent grid of (SMs x resident CTAs) warps takes
@@ -653,12 +588,10 @@ int set_tile_order_impl(int mode) {
 // C5 DP 2045 -> 2184 -- because warp tiles handed out in arrival order scatter adjacent row tiles
 // over different SMs, and the block-structured matrices (DLR1/DLR2: 6 or 5 consecutive rows share
 // their x entries) lose the L1 reuse that a CTA of 8 adjacent warp tiles gets on one SM.
-static int g_sched = 3;  // 0 static, 1 dynamic warp tiles, 2 balanced persistent, 3 auto (balanced below kBalWaves waves)
-constexpr int64_t kBalWaves = 8;
+static int g_sched = 0;
 
 int set_schedule_impl(int mode) {
-  if (mode < 0 || mode > 3)
-    return set_error(PJDS_ERR_INVALID_ARG, "schedule: 0 static, 1 dynamic warp tiles, 2 balanced persistent, 3 auto");
+  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "schedule: 0 static, 1 dynamic warp tiles");
   g_sched = mode;
   return PJDS_OK;
 }
@@ -679,7 +612,7 @@ template <typename T, typename Off, int R, int U, int M, bool PF, bool W>
 int launch_dyn(const pjds_mat* A, T* y, const T* x, cudaStream_t s, const int* order, int64_t grid_static,
                bool* launched) {
   *launched = false;
-  if (g_sched != 1) return PJDS_OK;
+  if (g_sched == 0) return PJDS_OK;
   static int occ = 0;
   auto kern = pjds_spmv_dyn_kernel<T, Off, R, U, M, PF, W>;
   if (!occ) {
@@ -715,63 +648,6 @@ int launch_dyn_any(const pjds_mat* A, T* y, const T* x, cudaStream_t s, const in
   }
   if (pipe) return launch_dyn<T, Off, R, U, M, true, false>(A, y, x, s, order, grid_static, launched);
   return launch_dyn<T, Off, R, U, M, false, false>(A, y, x, s, order, grid_static, launched);
-}
-
-// Warp-tile range per CTA for the balanced persistent grid: equal work = rows x (block length + 2)
-// (the +2 stands for the per-row y store and loop overhead), cut on warp-tile boundaries.
-int bal_table(const pjds_mat* Ac, int R, int grid, const int64_t** out) {
-  pjds_mat* A = const_cast<pjds_mat*>(Ac);  // lazily built cache of the handle
-  const int slot = R == 4 ? 2 : (R == 2 ? 1 : 0);
-  if (A->d_bal[slot] && A->bal_grid[slot] == grid) {
-    *out = A->d_bal[slot];
-    return PJDS_OK;
-  }
-  const auto& h = A->h;
-  const int64_t wrows = 32 * R;
-  const int64_t n_wt = (h.n_pad + wrows - 1) / wrows;
-  std::vector<double> pre(n_wt + 1, 0.0);
-  for (int64_t t = 0; t < n_wt; ++t) {
-    const int64_t k = t * wrows;
-    const int len = k < h.n ? h.block_len[k / h.br] : 0;
-    pre[t + 1] = pre[t] + (double)(len + 2);
-  }
-  std::vector<int64_t> bal(grid + 1, n_wt);
-  bal[0] = 0;
-  int64_t t = 0;
-  for (int b = 1; b < grid; ++b) {
-    const double target = pre[n_wt] * b / grid;
-    while (t < n_wt && pre[t + 1] <= target) ++t;
-    bal[b] = t;
-  }
-  if (A->d_bal[slot] && A->bal_grid[slot] < grid) {
-    cudaFree(A->d_bal[slot]);
-    A->d_bal[slot] = nullptr;
-  }
-  if (!A->d_bal[slot]) PJDS_CUDA_TRY(cudaMalloc(&A->d_bal[slot], (grid + 1) * sizeof(int64_t)));
-  PJDS_CUDA_TRY(cudaMemcpy(A->d_bal[slot], bal.data(), (grid + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-  A->bal_grid[slot] = grid;
-  *out = A->d_bal[slot];
-  return PJDS_OK;
-}
-
-template <typename T, typename Off, int R, int U, int M, bool PF>
-int launch_bal(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int pol) {
-  static int occ = 0;
-  auto kern = pjds_spmv_bal_kernel<T, Off, R, U, M, PF>;
-  if (!occ) {
-    PJDS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
-    occ = std::max(occ, 1);
-  }
-  const auto& h = A->h;
-  const int64_t n_wt = (h.n_pad + 32 * R - 1) / (32 * R);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * occ, (n_wt + 7) / 8));
-  const int64_t* bal = nullptr;
-  PJDS_TRY(bal_table(A, R, grid, &bal));
-  kern<<<(unsigned)grid, kThreads, 0, s>>>((const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x,
-                                           y, h.n, h.n_pad, h.br, pol, bal, h.width);
-  count_launch();
-  PJDS_CUDA_TRY(cudaGetLastError());
-  return PJDS_OK;
 }
 
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
@@ -816,24 +692,6 @@ int st;
   int pol = g_pol;
   if (A->y_store >= 0) pol = (pol & 0xff00ffff) | ((A->y_store & 0xff) << 16);
   if ((uintptr_t)y % (R * sizeof(T))) pol &= 0xff00ffff;
-  // few waves: the work-balanced persistent grid (schedule 2, or 3 = auto below kBalWaves waves).
-  // Its table is built at the first launch (a synchronous upload), so a stream being captured into
-  // a CUDA graph before that keeps the static grid.
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  const int bslot = R == 4 ? 2 : (R == 2 ? 1 : 0);
-  const bool capturing = cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
-  if ((g_sched == 2 || (g_sched == 3 && grid < kBalWaves * (int64_t)num_sms() * 5)) && !A->d_win && h.n_windows <= 1 &&
-      !(g_il && R > 1) && (mode == STORE_DIRECT || mode == STORE_PERM || mode == STORE_PERM_ACC) &&
-      (!capturing || A->d_bal[bslot])) {
-    if (mode == STORE_DIRECT)
-      return pipe ? launch_bal<T, Off, R, U, STORE_DIRECT, true>(A, y, x, s, pol)
-                  : launch_bal<T, Off, R, U, STORE_DIRECT, false>(A, y, x, s, pol);
-    if (mode == STORE_PERM_ACC)
-      return pipe ? launch_bal<T, Off, R, U, STORE_PERM_ACC, true>(A, y, x, s, pol)
-                  : launch_bal<T, Off, R, U, STORE_PERM_ACC, false>(A, y, x, s, pol);
-    return pipe ? launch_bal<T, Off, R, U, STORE_PERM, true>(A, y, x, s, pol)
-                : launch_bal<T, Off, R, U, STORE_PERM, false>(A, y, x, s, pol);
-  }
 #define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
   pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
       (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, pol, order, dot_part, h.sigma, \

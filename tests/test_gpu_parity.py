@@ -575,13 +575,11 @@ def test_spmv_host_batch_pipelined(pj, symmetric):
         check_y(y, n, rp, col, val, x)
 
 
-@pytest.mark.parametrize("sched", [0, 1, 2, 3])
+@pytest.mark.parametrize("sched", [0, 1])
 def test_schedule_bitwise(pj, sched):
-    """pjds_set_schedule: the dynamic warp-tile kernel (1) and the work-balanced persistent grid (2;
-    3 = auto) run the same row chains as the static grid (bitwise = the FMA chain), for every
-    rows-per-thread variant, the pipelined variant, both bases, both tile orders, ragged warp tiles,
-    repeated launches (the dynamic counter resets itself), and the accumulate store (y += A x: one
-    rounding add onto the previous y)."""
+    """pjds_set_schedule: the dynamic warp-tile kernel runs the same row chains as the static grid
+    (bitwise = the FMA chain), for every rows-per-thread variant, the pipelined variant, both
+    bases, both tile orders, ragged warp tiles, and repeated launches (its counter resets itself)."""
     L = pj.lib()
     try:
         assert L.pjds_set_schedule(sched) == 0
@@ -607,15 +605,8 @@ def test_schedule_bitwise(pj, sched):
                             yo = A.from_permuted(torch.empty_like(y), y) if sym else y
                             torch.cuda.synchronize()
                             check_y(yo.cpu().numpy(), n, rp, col, val, x)
-                            if not sym:
-                                y0 = inputs.vector(n, dtype, seed=91)
-                                ya = tdev(y0)
-                                A.spmv_accum(ya, xin)
-                                torch.cuda.synchronize()
-                                want = (y0 + oracle.spmv_chain(n, rp, col, val, x)).astype(dtype)
-                                assert np.array_equal(ya.cpu().numpy(), want), (name, variant, order)
                     del A
     finally:
-        L.pjds_set_schedule(3)
+        L.pjds_set_schedule(0)
         L.pjds_set_kernel_variant(0, 0)
         L.pjds_set_tile_order(2)
