@@ -605,6 +605,13 @@ def test_schedule_bitwise(pj, sched):
                             yo = A.from_permuted(torch.empty_like(y), y) if sym else y
                             torch.cuda.synchronize()
                             check_y(yo.cpu().numpy(), n, rp, col, val, x)
+                            if not sym:  # y += A x: one rounding add onto the previous y
+                                y0 = inputs.vector(n, dtype, seed=91)
+                                ya = tdev(y0)
+                                A.spmv_accum(ya, xin)
+                                torch.cuda.synchronize()
+                                want = (y0 + oracle.spmv_chain(n, rp, col, val, x)).astype(dtype)
+                                assert np.array_equal(ya.cpu().numpy(), want), (name, variant, order)
                     del A
     finally:
         L.pjds_set_schedule(0)

@@ -233,7 +233,7 @@ def test_round2_knobs_and_collective_create_validation(pj):
     assert L.pjds_set_dist_nl_sigma(1000) == -1 and L.pjds_set_dist_nl_sigma(-1024) == -1
     assert L.pjds_set_dist_nl_sigma(0) == 0 and L.pjds_set_dist_nl_sigma(2048) == 0
     assert L.pjds_set_dist_nl_sigma(1024) == 0  # back to the default
-    assert L.pjds_set_schedule(4) == -1 and L.pjds_set_schedule(3) == 0
+    assert L.pjds_set_schedule(2) == -1 and L.pjds_set_schedule(0) == 0
     assert L.pjds_set_tile_order(4) == -1 and L.pjds_set_tile_order(2) == 0
     n = 64
     _, rp, col, val = inputs.small("random", n, seed=2, max=9)
