@@ -61,7 +61,8 @@ def build_pjds(force: bool = False) -> str:
     out = os.path.join(ROOT, "paper_1112_5588_b200", "libpjds.so")
     if not (force or _stale(out, srcs + hdrs)):
         return out
-    cmd = [NVCC, "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fopenmp,-O3",
+    extra = os.environ.get("PJDS_NVCC_DEFINES", "").split()  # dev experiments (e.g. -DPJDS_CTA_THREADS=128)
+    cmd = [NVCC, "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fopenmp,-O3"] + extra + [
            "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xptxas", "-v",
            "-I", os.path.join(ROOT, "include"), "-I", _nccl_include(),
            "-o", out] + srcs + ["-lgomp", "-ldl", "-lcudart"]

@@ -203,7 +203,11 @@ __device__ __forceinline__ void load_rows(Vec<T, R>& v, const T* p, uint64_t pol
   }
 }
 
-constexpr int kThreads = 256;
+#ifndef PJDS_CTA_THREADS
+#define PJDS_CTA_THREADS 256
+#endif
+constexpr int kThreads = PJDS_CTA_THREADS;  // CTA size (build-time; a CTA tile is kThreads x R sorted rows)
+static_assert(kThreads % 32 == 0 && kThreads <= 256, "CTA size: a multiple of 32, at most 256");
 constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
 // Register budget: plain __launch_bounds__(256) (48 registers for the R=4 DP kernel).  Measured:
 // __launch_bounds__(256, 6) (<= 40 regs) is 3-15 % slower in DP, and __launch_bounds__(256, 1)
