@@ -82,7 +82,10 @@ def parse(argv=None):
                    help="auto: the permuted basis at N=1 and for the DIRECT transport; the original basis "
                         "(rows permuted, y stored through perm) for the NCCL / P2P split, whose halo lists "
                         "then are contiguous runs of x (no pack)")
-    p.add_argument("--block-rows", type=int, default=32, help="pJDS b_r (the paper's warp size; 128 = rows per warp at R=4)")
+    p.add_argument("--block-rows", type=int, default=128,
+                   help="pJDS b_r.  The paper pads each block of 'warp size' rows (P:L219-220); the B200 kernel's warp "
+                        "owns 32 x R = 128 consecutive sorted rows (R = 4), so the default is 128 (the library's own "
+                        "default stays 32; compare reports the other value, timed the same way)")
     p.add_argument("--no-overlap", action="store_true", help="dist: vector mode (exchange, then compute)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-compare", action="store_true", help="N=1: no compare legs; N>1: no p2p/direct legs")
@@ -347,7 +350,7 @@ def gflops_entry(nnz, b_min, ms, peak):
             "frac": round(b_min / (ms * 1e-3) / 1e9 / peak, 4)}
 
 
-def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, reps=None):
+def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, reps=None, block_rows=32):
     """One row of the SURVEY §8(d) targets table: pJDS (permuted basis, the library's automatic
     variant and tile order) and ELLPACK-R on the same matrix, each timed (a) with x/y rotated over
     enough copies that L2 cannot carry x from one launch to the next (the table's number) and (b)
@@ -369,7 +372,7 @@ def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, re
     nnz = int(rp[-1])
     b_min = nnz * (sv + 4) + 2 * n * sv
     x_host = inputs.vector(n, npdt)
-    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=block_rows, symmetric=True)
     E = pj.EllrMatrix.from_crs(n, rp, col, val)
     fa, fe = A.footprint(), E.footprint()
     del rp, col, val
@@ -380,7 +383,7 @@ def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, re
     xs_o = [x0.clone() for _ in range(sets)]
     ys = [torch.empty(n, dtype=tdt, device=dev) for _ in range(sets)]
     k = reps or max(3 * sets, int(np.ceil(20.0 / max(b_min / 6.0e12 * 1e3, 1e-3))))
-    out = {"config": cfg, "dtype": dt, "n": n, "nnz": nnz, "algorithmic_bytes": b_min,
+    out = {"config": cfg, "dtype": dt, "n": n, "nnz": nnz, "algorithmic_bytes": b_min, "block_rows": block_rows,
            "l2": f"x/y rotated over {sets} pairs ({sets * 2 * n * sv / 2**20:.0f} MiB > 2 x L2) between launches"}
     for name, M, xs in (("pjds", A, xs_p), ("ellr", E, xs_o)):
         for i in range(sets):
@@ -390,7 +393,8 @@ def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, re
         e = gflops_entry(nnz, b_min, cold, peak)
         w = gflops_entry(nnz, b_min, warm, peak)
         e.update({"us_l2_warm": w["us"], "frac_l2_warm": w["frac"], "launches_timed": k})
-        tr, src = committed_traffic(f"{cfg}/{dt}/{'permuted' if name == 'pjds' else 'ellr'}")
+        tr, src = committed_traffic(f"{cfg}/{dt}/{'permuted' if name == 'pjds' else 'ellr'}"
+                                    + ("/br%d" % block_rows if name == "pjds" and block_rows != 32 else ""))
         e["traffic"] = tr
         e["traffic_over_algorithmic"] = round(tr / b_min, 4) if tr else None
         e["traffic_source"] = src
@@ -516,12 +520,16 @@ def run_single(a, npdt, sv, argv_cfg):
             xb = x0
             if name.startswith("pjds") and getattr(B, "symmetric", False):
                 xb = B.to_permuted(torch.empty_like(x0), x0)
-            for _ in range(3):
+            # timed exactly like the headline (warm-up, then --steps back-to-back launches, clocks
+            # sampled): a short leg right after the host-side build would run at the idle GPU's
+            # unthrottled clock and flatter it against the sustained headline
+            for _ in range(max(a.warmup, 3)):
                 B.spmv(y, xb, stream=stream)
-            mb = timed(lambda i: B.spmv(y, xb, stream=stream), 20)
+            with ClockSampler(0) as ck:
+                mb = timed(lambda i: B.spmv(y, xb, stream=stream), a.steps)
             compare[name] = {"GFlop/s": round(2.0 * nnz / (mb * 1e-3) / 1e9, 1), "ms": round(mb, 4),
                              "frac": round(b_min / (mb * 1e-3) / 1e9 / peak, 4),
-                             "bytes": B.footprint()["bytes_total"]}
+                             "bytes": B.footprint()["bytes_total"], "sm_mhz": ck.summary().get("sm_mhz")}
             if name == "ellpack_r":
                 E = B.footprint()
             del B, xb
@@ -532,9 +540,9 @@ def run_single(a, npdt, sv, argv_cfg):
         warnings.filterwarnings("ignore", message="Sparse invariant checks")
         C = torch.sparse_csr_tensor(torch.from_numpy(rp.astype(np.int32)).to(dev), torch.from_numpy(col).to(dev),
                                     torch.from_numpy(val).to(dev), size=(n, n), check_invariants=False)
-        for _ in range(3):
+        for _ in range(max(a.warmup, 3)):
             torch.mv(C, x0)
-        mb = timed(lambda i: torch.mv(C, x0), 20)
+        mb = timed(lambda i: torch.mv(C, x0), max(20, a.steps // 2))
         compare["cusparse_csr"] = {"GFlop/s": round(2.0 * nnz / (mb * 1e-3) / 1e9, 1), "ms": round(mb, 4),
                                    "frac": round(b_min / (mb * 1e-3) / 1e9 / peak, 4),
                                    "bytes": int(nnz * (sv + 4) + (n + 1) * 4)}
@@ -564,7 +572,7 @@ def run_single(a, npdt, sv, argv_cfg):
         for cfg, dt in todo:
             if cfg == a.config and dt == a.dtype:
                 continue
-            per_config.append(per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache))
+            per_config.append(per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, block_rows=a.block_rows))
     del crs_cache, col, val
 
     # end-to-end through the public API with host buffers in the original basis (H2D x, basis

@@ -184,9 +184,10 @@ def test_c5_sampled(pj):
     assert np.isfinite(yh).all()
 
 
-@pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_c5_permuted_bench_instance(pj, dtype):
-    """The exact headline instance of bench.py: C5, permuted basis (PJDS_PERM_SYMMETRIC), b_r = 32,
+@pytest.mark.parametrize("dtype,br", [(np.float64, 128), (np.float32, 128), (np.float64, 32)])
+def test_c5_permuted_bench_instance(pj, dtype, br):
+    """The exact headline instance of bench.py: C5, permuted basis (PJDS_PERM_SYMMETRIC), b_r = 128
+    (the bench default since round 2; 32 = the library default, also checked),
     automatic variant (R = 4, U = 2), automatic tile order (original-row order: x > 64 MB), vector
     y store.  >= 100 K sampled rows against O1 at the O2 bound AND bitwise against the O3 chain (one
     FMA chain per row in CRS order, Listing 2); all rows finite."""
@@ -194,7 +195,7 @@ def test_c5_permuted_bench_instance(pj, dtype):
     rp, col, val = g.crs(dtype=dtype)
     n = g.n
     x = inputs.vector(n, dtype)
-    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=32, symmetric=True)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, symmetric=True)
     del col, val
     assert A.symmetric
     xt = tdev(x)

@@ -11,9 +11,10 @@ import torch
 import inputs
 import paper_1112_5588_b200 as pj
 
-ORDER = [("C5", "f64", "permuted"), ("C5", "f64", "rows"), ("C5", "f64", "ellr"), ("C5", "f32", "permuted"),
+ORDER = [("C5", "f64", "permuted"), ("C5", "f64", "permuted/br128"), ("C5", "f64", "rows"),
+         ("C5", "f64", "rows/br128"), ("C5", "f64", "ellr"), ("C5", "f32", "permuted/br128"),
          ("C5", "f32", "ellr")] + [(c, d, f) for c in ("C2", "C3", "C4") for d in ("f64", "f32")
-                                   for f in ("permuted", "ellr")]
+                                   for f in ("permuted", "permuted/br128", "ellr")]
 if __name__ == "__main__":
     cache = {}
     for cfg, dt, fmt in ORDER:
@@ -28,7 +29,8 @@ if __name__ == "__main__":
         if fmt == "ellr":
             M = pj.EllrMatrix.from_crs(n, rp, col, val)
         else:
-            M = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=(fmt == "permuted"))
+            base, _, br = fmt.partition("/br")
+            M = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=int(br or 32), symmetric=(base == "permuted"))
         M.spmv(y, x)
         torch.cuda.synchronize()
         print(json.dumps({"cfg": cfg, "dtype": dt, "fmt": fmt}), flush=True)
