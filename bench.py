@@ -676,8 +676,8 @@ def gather_rows(dist, rank, rows_global, y_orig_loc, lo, hi):
     """Every rank's values of the sampled rows it owns -> rank 0 (setup-time plumbing)."""
     mine = rows_global[(rows_global >= lo) & (rows_global < hi)]
     vals = y_orig_loc[mine - lo] if len(mine) else y_orig_loc[:0]
-    objs = [None] * dist.get_world_size() if rank == 0 else None
-    dist.gather_object((mine, vals), objs, dst=0)
+    objs = [None] * dist.get_world_size()
+    dist.all_gather_object(objs, (mine, vals))  # small (~100 K values in total); works on gloo and NCCL
     if rank != 0:
         return None
     idx = np.concatenate([o[0] for o in objs])
