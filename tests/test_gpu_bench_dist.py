@@ -33,7 +33,7 @@ def test_bench_gpus_oversubscribed(cfg, gpus, basis):
     assert d["parity"]["within_bound"] and d["parity"]["gpu_finite_all_rows"], d["parity"]
     assert d["parity"]["rows_checked"] >= 1000
     di = d["dist"]
-    assert di["oversubscribed"] and "m6_task_gain_le_2" in di and di["t1_ms"] > 0
+    assert di["oversubscribed"] and di["m6_task_gain_le_2"] is None and di["t1_ms"] > 0
     assert di["parallel_efficiency_vs_t1"] is not None
     for trn in ("p2p", "direct"):
         leg = di["transports"][trn]
