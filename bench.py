@@ -98,6 +98,8 @@ def parse(argv=None):
     p.add_argument("--tile-window", type=int, default=0,
                    help="HMEp configs, N=1: run tiles by (phonon window of this many rows, original row); 0 = off")
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
+    p.add_argument("--variant", default="", metavar="R,U",
+                   help="kernel variant knob (pjds_set_kernel_variant; default: the library's automatic choice)")
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
     p.add_argument("--transport", default="nccl", choices=["nccl", "p2p", "direct"],
                    help="dist: NCCL send/recv on a side stream, the fused gather+put P2P kernel, or DIRECT "
@@ -428,6 +430,10 @@ def run_single(a, npdt, sv, argv_cfg):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     tdt = torch.float64 if npdt == np.float64 else torch.float32
+    if a.variant:
+        vr, vu = (int(v) for v in a.variant.split(","))
+        if pj.lib().pjds_set_kernel_variant(vr, vu) != 0:
+            raise SystemExit(f"bench.py: bad --variant {a.variant}")
     t_setup = time.perf_counter()
     g = inputs.Generator.from_config(a.config)
     n = g.n
@@ -642,6 +648,7 @@ def run_single(a, npdt, sv, argv_cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": a.dtype,
         "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
         "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows, "parallelism": "single GPU",
+                   "variant": a.variant or "auto",
                    "overlap": None, "transport": None, "tile_window": a.tile_window or None,
                    "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
         "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),

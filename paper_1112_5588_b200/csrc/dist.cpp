@@ -189,15 +189,20 @@ size_t vsz(const pjds_dist* D) { return dtype_size(D->dtype); }
 int post_nccl(pjds_dist* D, const void* x_loc, cudaStream_t s) {
   const size_t vs = vsz(D);
   NCCL_TRY(g_nccl.groupStart());
+  ncclResult_t r = ncclSuccess;
   for (auto& ps : D->sends) {
     const char* base = ps.packed ? (const char*)D->d_packbuf : (const char*)x_loc;
-    for (auto& r : ps.runs)
-      NCCL_TRY(g_nccl.send(base + r.first * vs, (size_t)r.second, nccl_type(D->dtype), ps.peer, D->nccl, s));
+    for (auto& run : ps.runs)
+      if (r == ncclSuccess)
+        r = g_nccl.send(base + run.first * vs, (size_t)run.second, nccl_type(D->dtype), ps.peer, D->nccl, s);
   }
   for (auto& pr : D->recvs)
-    for (auto& r : pr.runs)
-      NCCL_TRY(g_nccl.recv((char*)D->d_halo + r.first * vs, (size_t)r.second, nccl_type(D->dtype), pr.peer, D->nccl, s));
-  NCCL_TRY(g_nccl.groupEnd());
+    for (auto& run : pr.runs)
+      if (r == ncclSuccess)
+        r = g_nccl.recv((char*)D->d_halo + run.first * vs, (size_t)run.second, nccl_type(D->dtype), pr.peer, D->nccl, s);
+  const ncclResult_t e = g_nccl.groupEnd();  // the group is closed even when a post failed
+  if (r != ncclSuccess) return set_error(PJDS_ERR_NCCL, std::string("ncclSend/ncclRecv: ") + g_nccl.errStr(r));
+  if (e != ncclSuccess) return set_error(PJDS_ERR_NCCL, std::string("ncclGroupEnd: ") + g_nccl.errStr(e));
   return PJDS_OK;
 }
 
@@ -425,7 +430,9 @@ int pjds_dist_create_crs(pjds_dist_t* out, const void* nccl_id, int32_t nranks, 
   int32_t* d_ids = nullptr;  // [halo + send_total]
   std::vector<int64_t> sc(nranks, 0);
   std::vector<int32_t> scols;
+  bool in_group = false;  // a failure between ncclGroupStart and ncclGroupEnd still closes the group
   auto cleanup = [&](int status) {
+    if (in_group) g_nccl.groupEnd();
     if (st) cudaStreamDestroy(st);
     cudaFree(d_cnt);
     cudaFree(d_ids);
@@ -455,11 +462,13 @@ int pjds_dist_create_crs(pjds_dist_t* out, const void* nccl_id, int32_t nranks, 
     // 1. counts: my recv count from q goes to q, q's recv count from me comes back as my send count
     ncclResult_t rr;
     if ((rr = g_nccl.groupStart()) != ncclSuccess) return nccl_fail(rr, "ncclGroupStart");
+    in_group = true;
     for (int q = 0; q < R; ++q) {
       if (q == rank) continue;
       if ((rr = g_nccl.send(d_cnt + q, 1, ncclInt64, q, comm, st)) != ncclSuccess) return nccl_fail(rr, "ncclSend");
       if ((rr = g_nccl.recv(d_cnt + R + q, 1, ncclInt64, q, comm, st)) != ncclSuccess) return nccl_fail(rr, "ncclRecv");
     }
+    in_group = false;
     if ((rr = g_nccl.groupEnd()) != ncclSuccess) return nccl_fail(rr, "ncclGroupEnd");
     if (cudaStreamSynchronize(st) != cudaSuccess ||
         cudaMemcpy(sc.data(), d_cnt + R, R * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -475,6 +484,7 @@ int pjds_dist_create_crs(pjds_dist_t* out, const void* nccl_id, int32_t nranks, 
         (halo && cudaMemcpy(d_ids, P->recv_cols.data(), halo * 4, cudaMemcpyHostToDevice) != cudaSuccess))
       return cleanup(set_error(PJDS_ERR_OOM, "pjds_dist_create_crs: id buffers"));
     if ((rr = g_nccl.groupStart()) != ncclSuccess) return nccl_fail(rr, "ncclGroupStart");
+    in_group = true;
     int64_t ro = 0, so = halo;
     for (int q = 0; q < R; ++q) {
       const int64_t rc = P->recv_counts[q];
@@ -485,6 +495,7 @@ int pjds_dist_create_crs(pjds_dist_t* out, const void* nccl_id, int32_t nranks, 
       ro += rc;
       so += sc[q];
     }
+    in_group = false;
     if ((rr = g_nccl.groupEnd()) != ncclSuccess) return nccl_fail(rr, "ncclGroupEnd");
     scols.resize(send_total);
     if (cudaStreamSynchronize(st) != cudaSuccess ||
