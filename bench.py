@@ -415,6 +415,7 @@ def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, re
                         "data_reduction_vs_ellpack": round(A.info["data_reduction_vs_ellpack"], 5)}
     # the paper's "performance between 95 % and 130 % of ELLPACK-R"
     out["pjds_perf_over_ellr"] = round(out["ellr"]["us"] / out["pjds"]["us"], 4)
+    out["paper_pjds_perf_over_ellr"] = "0.95-1.30 on Fermi C2070 (PAPER.md L19-22, Table 1 L292-295)"
     out["pjds_perf_over_ellr_l2_warm"] = round(out["ellr"]["us_l2_warm"] / out["pjds"]["us_l2_warm"], 4)
     del A, E, xs_p, xs_o, ys, x0, xp
     torch.cuda.synchronize()
