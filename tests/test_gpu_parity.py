@@ -243,12 +243,20 @@ def test_symmetric_mode(pj):
 
 @pytest.mark.parametrize("R", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("permuted", [False, True])
-def test_dist_group_random(pj, R, permuted):
+@pytest.mark.parametrize("nl_sigma,br", [(1024, 32), (0, 32), (2048, 128)])
+def test_dist_group_random(pj, R, permuted, nl_sigma, br):
+    """The split path against the O5 emulator, bitwise: A_nl in y-target order with 1024 / 2048-row
+    sort windows (the default, reading 27) or globally sorted, b_r 32 and 128."""
     n = 4000
     _, rp, col, val = inputs.small("random", n, seed=R, max=50)
     x = inputs.vector(n)
     offs = np.array([n * r // R for r in range(R + 1)], np.int64)
-    hs = pj.DistPjds.create_group(n, rp, col, val, offs, permuted=permuted)
+    L = pj.lib()
+    assert L.pjds_set_dist_nl_sigma(nl_sigma) == 0
+    try:
+        hs = pj.DistPjds.create_group(n, rp, col, val, offs, permuted=permuted, block_rows=br)
+    finally:
+        L.pjds_set_dist_nl_sigma(1024)
     xs = [tdev(x[offs[r]:offs[r + 1]]) for r in range(R)]
     if permuted:
         xs = [h.to_permuted(torch.empty_like(v), v) for h, v in zip(hs, xs)]
@@ -513,6 +521,12 @@ def test_y_store_bitwise(pj, y_kind, variant):
                 y = np.empty(n, dtype)
                 A.spmv_host(y, x)
                 check_y(y, n, rp, col, val, x)
+                # the per-handle override (pjds_set_y_store) with every kind, on top of the global one
+                for ys in (-1, 0, 1, 2, 3, 4):
+                    assert L.pjds_set_y_store(A._h, ys) == 0
+                    y = np.empty(n, dtype)
+                    A.spmv_host(y, x)
+                    check_y(y, n, rp, col, val, x)
     finally:
         L.pjds_set_cache_policy(1 | (2 << 8), 2)
         L.pjds_set_kernel_variant(0, 0)
