@@ -5,12 +5,12 @@
 set -u
 mkdir -p gpurun_out/scale
 NG=$(python -c "import torch; print(torch.cuda.device_count())")
-timeout 900 python bench.py --steps 100 --warmup 5 --no-compare > gpurun_out/scale/n1.json 2> gpurun_out/scale/n1.err
+timeout 900 python bench.py --steps 100 --warmup 5 --no-compare --no-per-config > gpurun_out/scale/n1.json 2> gpurun_out/scale/n1.err
 for N in 2 4 8; do
   [ "$N" -le "$NG" ] || continue
-  for TR in nccl p2p direct; do
-    timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$N" --master-addr 127.0.0.1 \
-      --master-port $((29900 + N * 3 + ${#TR})) bench.py --gpus "$N" --steps 100 --warmup 5 --transport "$TR" \
+  # bench.py --gpus N launches its own N ranks (torchrun) and times the other transports as legs
+  for TR in nccl direct; do
+    timeout 1200 python bench.py --gpus "$N" --steps 100 --warmup 5 --transport "$TR" \
       > "gpurun_out/scale/n${N}_${TR}.json" 2> "gpurun_out/scale/n${N}_${TR}.err"
     echo "N=$N transport=$TR rc=$?"
   done
