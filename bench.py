@@ -673,6 +673,12 @@ def run_single(a, npdt, sv, argv_cfg):
         "compare": compare or None,
         "per_config": per_config,
         "dist": None,
+        # the paper's own numbers, for context only (other hardware, real matrices)
+        "paper_context": {"hardware": "Tesla C2070 (Fermi), ECC on for DP; streaming bandwidth 91 GB/s with ECC "
+                                      "(PAPER.md L68-70)",
+                          "pjds_dp_gflops": {"HMEp": 7.5, "sAMG": 8.5, "DLR1": 12.9, "DLR2": 9.5},
+                          "ellpack_r_dp_gflops": {"HMEp": 7.9, "sAMG": 7.8, "DLR1": 12.9, "DLR2": 9.6},
+                          "source": "PAPER.md Table 1 L292-295"},
         "setup_s": round(t_setup, 2),
     }
     print(json.dumps(out), flush=True)
