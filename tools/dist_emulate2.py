@@ -37,6 +37,7 @@ p.add_argument("--pstore", default="0", help="comma list of perm-store kinds for
 p.add_argument("--all-ranks", action="store_true", help="emulate every rank (default: ranks 0 and R/2)")
 p.add_argument("--reps", type=int, default=20)
 p.add_argument("--nl-sigma", default="1024", help="comma list of A_nl sort scopes (pjds_set_dist_nl_sigma)")
+p.add_argument("--nl-variants", default="", help="comma list RxU: time A_nl alone under each kernel variant")
 a = p.parse_args()
 SEG = {"C1": 1024, "C3": 15504, "C5": 142506}[a.config]
 npdt = np.float64 if a.dtype == "f64" else np.float32
@@ -123,11 +124,18 @@ for mode, R, nls in [(m_, r_, s_) for m_ in a.modes.split(",") for r_ in map(int
                     t_pack = timeit(lambda: torch.index_select(x, 0, idx, out=packbuf), a.reps) if idx is not None else 0.0
 
                     t_nl = timeit(lambda: A_nl.spmv_accum(y, halo), a.reps) if A_nl is not None else 0.0
+                    nl_var = {}
+                    for v in [q for q in a.nl_variants.split(",") if q]:
+                        vr, vu = map(int, v.split("x"))
+                        pj.lib().pjds_set_kernel_variant(vr, vu)
+                        nl_var[v] = round(timeit(lambda: A_nl.spmv_accum(y, halo), a.reps) * 1e6, 1) if A_nl is not None else 0.0
+                    pj.lib().pjds_set_kernel_variant(0, 0)
                     t_link = t_pack + xb / 2 / B_LINK + t_nl  # one direction's bytes over NVLink
                     ranks.append({"rank": r, "t_unit_us": t_unit * 1e6, "t_loc_us": t_loc * 1e6,
                                   "t_nl_us": t_nl * 1e6, "t_side_us": t_side * 1e6, "t_pack_us": t_pack * 1e6,
                                   "t_link_path_us": t_link * 1e6, "t_rank_us": max(t_unit, t_link) * 1e6,
-                                  "halo": h.info["halo"], "packed_send": npk, "rows_nl": h.info["rows_nonlocal"]})
+                                  "halo": h.info["halo"], "packed_send": npk, "rows_nl": h.info["rows_nonlocal"],
+                                  "t_nl_by_variant_us": nl_var or None})
                     pj.lib().pjds_set_y_store(A_loc._h, -1)
                     del src, dst, x, y, halo, packbuf
                 tmax = max(rr["t_rank_us"] for rr in ranks)
