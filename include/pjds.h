@@ -467,6 +467,16 @@ int pjds_set_tile_order(int32_t mode);
    handle must not run on two streams at once under the dynamic schedule.  Not used by the
    Lanczos-fused product, sigma-windowed handles or the lane-interleaved variant. */
 int pjds_set_schedule(int32_t mode);
+/* pjds_set_launch_overlap (process-wide knob; results are identical): programmatic dependent launch
+   of the pJDS y = A x / y += A x kernel and the ELLPACK-R kernel.  mode 1: launched with
+   cudaLaunchAttributeProgrammaticStreamSerialization, a product's CTAs may start while the previous
+   kernel on the stream drains its last wave; they run the matrix-only prologue and wait
+   (griddepcontrol.wait) for that kernel to complete before reading x or writing y, so the stream
+   order of an iterative scheme is kept.  prefetch_cols > 0: first-wave warps
+   also prefetch the first prefetch_cols jagged columns of their val/col rows into L2 (global sort
+   only) before waiting.  mode 0 (the library default): plain launches.  Errors: INVALID_ARG for
+   mode outside {0, 1} or prefetch_cols outside [0, 64]. */
+int pjds_set_launch_overlap(int32_t mode, int32_t prefetch_cols);
 
 /* Number of kernel launches this library has enqueued (process-wide counter). */
 int64_t pjds_launch_count(void);

@@ -114,6 +114,7 @@ _SIGS = {
     "pjds_set_y_store": [c_p, c_i32],
     "pjds_set_tile_order": [c_i32],
     "pjds_set_schedule": [c_i32],
+    "pjds_set_launch_overlap": [c_i32, c_i32],
     "pjds_set_tile_keys": [c_p, c_p, c_i64],
     "pjds_lanczos": [c_p, c_p, c_i32, c_p, c_p, c_p, c_p],
     "pjds_tridiag_eigenvalues": [c_i32, c_p, c_p, c_p],

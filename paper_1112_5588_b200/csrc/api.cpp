@@ -484,6 +484,7 @@ int pjds_set_y_store(pjds_t A, int32_t kind) {
 }
 int pjds_set_tile_order(int32_t mode) { return set_tile_order(mode); }
 int pjds_set_schedule(int32_t mode) { return set_schedule(mode); }
+int pjds_set_launch_overlap(int32_t mode, int32_t prefetch_cols) { return set_launch_overlap(mode, prefetch_cols); }
 
 int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n) {
   if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: NULL handle");

@@ -148,6 +148,7 @@ int set_kernel_variant(int r, int u);
 int set_cache_policy(int stream_kind, int x_kind);
 int set_tile_order(int mode);
 int set_schedule(int mode);
+int set_launch_overlap(int mode, int prefetch_cols);
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
 void count_launch(int64_t k = 1);
 }  // namespace pjds

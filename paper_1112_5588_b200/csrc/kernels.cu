@@ -219,6 +219,38 @@ constexpr int kSmemCS = 1024;  // col_start entries staged in shared memory
 // is the input entry of row k): the Lanczos alpha = (A v).v fused into the product's epilogue.
 enum { STORE_PERM = 0, STORE_DIRECT = 1, STORE_PERM_ACC = 2, STORE_DIRECT_DOT = 3 };
 
+// ---- programmatic dependent launch (sm_90+; B200 launch overlap of back-to-back products) -----
+// A product launched with cudaLaunchAttributeProgrammaticStreamSerialization may start while the
+// previous grid on the stream drains: its CTAs run the matrix-only prologue (tile/warp lookup,
+// col_start staging, and -- first-wave CTAs only -- an L2 prefetch of the first jagged columns of
+// their val/col tiles) and then block in griddepcontrol.wait until the previous grid has completed
+// and its writes are visible.  x, y and dot_part are touched only after the wait, so any producer /
+// consumer order of an iterative scheme is kept.  Launched without the attribute both instructions
+// are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+               : "memory");
+}
+// lane j < ncols of the warp prefetches the warp's rows [warp_k0, warp_k0 + 32R) of jagged column j
+// (val and col; column j holds sorted rows [0, col_start[j+1] - col_start[j]) of a global sort).
+// Ranges are 16-byte aligned multiples of 16 bytes: col_start entries are multiples of b_r (>= 32)
+// and warp_k0 a multiple of 32R.
+template <typename T, typename Off, int R>
+__device__ __forceinline__ void pdl_prefetch_warp(const T* val, const int* col, const Off* s_cs,
+                                                  const int64_t* col_start, int64_t warp_k0, int ncols, uint64_t pol) {
+  const int j = threadIdx.x & 31;
+  if (j >= ncols) return;
+  const int64_t c0 = j < kSmemCS ? (int64_t)s_cs[j] : col_start[j];
+  const int64_t c1 = j + 1 < kSmemCS ? (int64_t)s_cs[j + 1] : col_start[j + 1];
+  int64_t m = c1 - c0 - warp_k0;  // rows of the warp present in column j
+  if (m <= 0) return;
+  if (m > 32 * R) m = 32 * R;
+  prefetch_l2_bulk(val + c0 + warp_k0, (uint32_t)(m * sizeof(T)), pol);
+  prefetch_l2_bulk(col + c0 + warp_k0, (uint32_t)(m * sizeof(int)), pol);
+}
+
 // ---- pJDS kernel -----------------------------------------------------------------------------
 
 // The R row chains of one thread (rows k0 + r*RS, all of length `len`, one jagged column per
@@ -329,7 +361,10 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
                  double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off,
                  const T* const* __restrict__ win, int win_shift, const int* __restrict__ warp_order,
-                 int64_t n_wtiles) {
+                 int64_t n_wtiles, int pf_cols, int pf_ctas) {
+  // programmatic dependent launch (see pdl_prologue): the next grid on the stream may be scheduled
+  // once every CTA of this one has started, i.e. into the SM slots this grid's last wave frees
+  pdl_trigger();
   __shared__ Off s_cs[kSmemCS];
   __shared__ const T* s_win[WIN ? kMaxWin : 1];
   if constexpr (WIN)
@@ -365,9 +400,13 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   T acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = T(0);
-  if (active) {
   const int64_t warp_k0 = IL ? (k0 - (threadIdx.x & 31)) : (k0 - (int64_t)(threadIdx.x & 31) * R);
-  const int wlen = block_len[warp_k0 / br];
+  const int wlen = active ? block_len[warp_k0 / br] : 0;
+  // everything above reads only the matrix; x (and y, dot_part) only after the previous grid is done
+  if (pf_cols > 0 && (int)blockIdx.x < pf_ctas && active)
+    pdl_prefetch_warp<T, Off, R>(val, col, s_cs, col_start, warp_k0, min(wlen, pf_cols), make_policy(pol & 0xff));
+  pdl_wait();
+  if (active) {
   const int len = (br >= 32 * R) ? wlen : block_len[k0 / br];
   const uint64_t pol_s = make_policy(pol & 0xff);
   const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
@@ -654,6 +693,40 @@ int launch_dyn_any(const pjds_mat* A, T* y, const T* x, cudaStream_t s, const in
   return launch_dyn<T, Off, R, U, M, false, false>(A, y, x, s, order, grid_static, launched);
 }
 
+// Programmatic dependent launch of the static pJDS kernel (pjds_set_launch_overlap): 0 off, 1 on;
+// g_pdl_pf = jagged columns of its val/col tile a first-wave warp prefetches into L2 while the
+// previous grid drains (0 = none).
+static int g_pdl = 0, g_pdl_pf = 0;
+
+// first-wave CTA count of a kernel (SMs x resident CTAs), cached per kernel
+template <typename K>
+static int first_wave_ctas(K kern) {
+  static int v = 0;
+  if (!v) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+    v = num_sms() * occ;
+  }
+  return v;
+}
+
+// launch with or without cudaLaunchAttributeProgrammaticStreamSerialization
+template <typename... P, typename... A>
+static int launch_ex(void (*kern)(P...), int64_t grid, cudaStream_t s, bool pdl, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  PJDS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+  return PJDS_OK;
+}
+
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
 static bool g_il = false;    // lane-interleaved rows (variant knob unroll + 32; needs b_r % (32 R) == 0)
 
@@ -696,10 +769,16 @@ int st;
   int pol = g_pol;
   if (A->y_store >= 0) pol = (pol & 0xff00ffff) | ((A->y_store & 0xff) << 16);
   if ((uintptr_t)y % (R * sizeof(T))) pol &= 0xff00ffff;
-#define PJDS_LAUNCH_W(M, PF, IL, W)                                                                     \
-  pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W><<<(unsigned)grid, kThreads, 0, s>>>(                     \
-      (const T*)A->d_val, A->d_col, A->d_col_start, A->d_block_len, A->d_perm, x, y, h.n, h.n_pad, h.br, pol, order, dot_part, h.sigma, \
-      A->d_wcs_off, (const T* const*)A->d_win, A->win_shift, worder, n_wtiles)
+  // programmatic dependent launch for y = A x / y += A x (not the Lanczos dot product, whose
+  // launches are captured into a graph with its reduce passes)
+  const bool pdl = g_pdl && mode != STORE_DIRECT_DOT;
+  const int pf_cols = pdl && h.n_windows <= 1 ? g_pdl_pf : 0;
+#define PJDS_LAUNCH_W(M, PF, IL, W)                                                                      \
+  PJDS_TRY(launch_ex(pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W>, grid, s, pdl,                          \
+      (const T*)A->d_val, (const int*)A->d_col, (const int64_t*)A->d_col_start, (const int*)A->d_block_len, \
+      (const int*)A->d_perm, x, y, h.n, h.n_pad, (int)h.br, pol, order, dot_part, h.sigma,                  \
+      (const int64_t*)A->d_wcs_off, (const T* const*)A->d_win, (int)A->win_shift, worder, n_wtiles, pf_cols, \
+      pf_cols > 0 ? first_wave_ctas(pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W>) : 0))
 #define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
   if (A->d_win) {  // fused remote-gather dist matrix: plain main loop, direct or perm store
     if constexpr (std::is_same<Off, int32_t>::value) {
@@ -814,12 +893,14 @@ template <typename T, int R, int U>
 __global__ void __launch_bounds__(kThreads)
 ellr_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int* __restrict__ rowmax,
                  const T* __restrict__ x, T* __restrict__ y, int64_t n, int64_t n_pad) {
+  pdl_trigger();  // programmatic dependent launch, as in the pJDS kernel (no prefetch)
   const int64_t i0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * R;
   if (i0 >= n_pad) return;
   const uint64_t pol_s = policy_evict_first();
   const uint64_t pol_x = policy_evict_last();
   Vec<int, R> lens;
   lens.load(rowmax + i0, pol_s);
+  pdl_wait();
   int tmax = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) tmax = max(tmax, lens.v[r]);
@@ -940,6 +1021,13 @@ int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t
 
 int set_tile_order(int mode) { return set_tile_order_impl(mode); }
 int set_schedule(int mode) { return set_schedule_impl(mode); }
+int set_launch_overlap(int mode, int prefetch_cols) {
+  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: mode 0 off, 1 programmatic dependent launch");
+  if (prefetch_cols < 0 || prefetch_cols > 64) return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: prefetch_cols in [0, 64]");
+  g_pdl = mode;
+  g_pdl_pf = prefetch_cols;
+  return PJDS_OK;
+}
 
 int set_cache_policy(int stream_kind, int x_kind) {
   // bits 8-15 of stream_kind: y store of the permuted-basis kernel (0 plain scalar stores,
@@ -992,8 +1080,8 @@ int launch_ellr_t(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
   const auto& h = A->h;
   const int64_t grid = (h.n_pad / R + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
-  ellr_spmv_kernel<T, R, U><<<(unsigned)grid, kThreads, 0, s>>>((const T*)A->d_val, A->d_col, A->d_rowmax,
-                                                                (const T*)x, (T*)y, h.n, h.n_pad);
+  PJDS_TRY(launch_ex(ellr_spmv_kernel<T, R, U>, grid, s, g_pdl != 0, (const T*)A->d_val, (const int*)A->d_col,
+                     (const int*)A->d_rowmax, (const T*)x, (T*)y, h.n, h.n_pad));
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;

@@ -632,3 +632,66 @@ def test_schedule_bitwise(pj, sched):
         L.pjds_set_schedule(0)
         L.pjds_set_kernel_variant(0, 0)
         L.pjds_set_tile_order(2)
+
+
+@pytest.mark.parametrize("overlap", [(1, 0), (1, 4), (1, 64)])
+def test_launch_overlap_dependent_chain(pj, overlap):
+    """pjds_set_launch_overlap: a product launched as a programmatic dependent of the previous one
+    starts in its tail but reads x and writes y only after griddepcontrol.wait, so a chain of
+    dependent products x_{k+1} = A x_k over two ping-pong buffers (product k+1 overwrites the x that
+    product k reads: RAW and WAR on every step) gives, bitwise, the oracle's chain of FMA chains --
+    for the pJDS kernel (row-only and permuted basis, tile orders 0/1/3, every rows-per-thread
+    variant, widths past the 1024 staged col_start entries), y += A x, and ELLPACK-R."""
+    L = pj.lib()
+    try:
+        assert L.pjds_set_launch_overlap(*overlap) == 0
+        cases = [("C1", None), ("C4", None), ("random", 1500), ("adversarial", 3000), ("empty_rows", 513)]
+        for name, m in cases:
+            for dtype in (np.float64, np.float32):
+                if m is None:
+                    n, rp, col, val = inputs.config_crs(name, dtype=dtype)
+                else:
+                    n, rp, col, val = inputs.small(name, m, seed=m, dtype=dtype, **({"max": 90} if name == "random" else {}))
+                # scale the values so that 6 products stay O(1) (exact: a power of two)
+                val = (val * dtype(2.0 ** -4)).astype(dtype)
+                x0 = inputs.vector(n, dtype)
+                want = [x0]
+                for _ in range(6):
+                    want.append(oracle.spmv_chain(n, rp, col, val, want[-1]))
+                for sym in (False, True):
+                    A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=sym, block_rows=128 if n > 2000 else 32)
+                    for variant in ((0, 0), (1, 8), (2, 4), (4, 2)):
+                        assert L.pjds_set_kernel_variant(*variant) == 0
+                        for order in (0, 1, 3):
+                            assert L.pjds_set_tile_order(order) == 0
+                            b = [tdev(x0), torch.full_like(tdev(x0), float("nan"))]
+                            if sym:
+                                b[0] = A.to_permuted(torch.empty_like(b[0]), b[0])
+                            for k in range(6):
+                                A.spmv(b[(k + 1) % 2], b[k % 2])
+                            out = b[0]
+                            if sym:
+                                out = A.from_permuted(torch.empty_like(out), out)
+                            torch.cuda.synchronize()
+                            assert np.array_equal(out.cpu().numpy(), want[6]), (name, dtype, sym, variant, order)
+                    if not sym:  # y += A x, three times onto the same y (each depends on the previous)
+                        assert L.pjds_set_kernel_variant(0, 0) == 0
+                        ya = tdev(x0)
+                        xt = tdev(want[1])
+                        acc = x0.copy()
+                        for _ in range(3):
+                            A.spmv_accum(ya, xt)
+                            acc = (acc + want[2]).astype(dtype)
+                        torch.cuda.synchronize()
+                        assert np.array_equal(ya.cpu().numpy(), acc), (name, dtype, "accum")
+                    del A
+                E = pj.EllrMatrix.from_crs(n, rp, col, val)
+                b = [tdev(x0), torch.full_like(tdev(x0), float("nan"))]
+                for k in range(6):
+                    E.spmv(b[(k + 1) % 2], b[k % 2])
+                torch.cuda.synchronize()
+                assert np.array_equal(b[0].cpu().numpy(), want[6]), (name, dtype, "ellr")
+    finally:
+        L.pjds_set_launch_overlap(0, 0)
+        L.pjds_set_kernel_variant(0, 0)
+        L.pjds_set_tile_order(2)

@@ -34,6 +34,8 @@ p.add_argument("--sigmas", default="0")
 p.add_argument("--keys", default="none", help="tile keys: none (original index) or wW = HMEp phonon window of W rows")
 SEG = {"C1": 1024, "C3": 15504, "C5": 142506}
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
+p.add_argument("--pdls", default="0:0", help="launch overlap mode:prefetch_cols list (pjds_set_launch_overlap)")
+p.add_argument("--rotate", type=int, default=1, help="x/y pairs cycled over the timed launches (L2 carry-over)")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
 pj.bw_probe(1 << 30, 20)  # bring the GPU out of its idle clocks before the first measurement
@@ -45,6 +47,8 @@ for cfg in a.configs.split(","):
         nnz = len(col)
         x = torch.from_numpy(inputs.vector(n, npdt)).cuda()
         y = torch.empty_like(x)
+        xs = [x] + [x.clone() for _ in range(a.rotate - 1)]
+        ys = [y] + [torch.empty_like(x) for _ in range(a.rotate - 1)]
         bmin = nnz * (sv + 4) + 2 * n * sv
         for fmt, sg in [(f, g) for f in a.fmts.split(",") for g in (a.sigmas.split(",") if f.startswith("pjds") else ["0"])]:
           if fmt.startswith("pjds"):
@@ -54,10 +58,12 @@ for cfg in a.configs.split(","):
           else:
               A = pj.EllrMatrix.from_crs(n, rp, col, val)
           pj.bw_probe(1 << 30, 20)  # host-side conversion leaves the GPU idle: re-raise clocks
-          for var, polk, order, kspec, sch in [(v, q, o, kk, sc) for v in a.variants.split(",") for q in a.policies.split(",")
+          for var, polk, order, kspec, sch, pdl in [(v, q, o, kk, sc, pd) for v in a.variants.split(",") for q in a.policies.split(",")
                                                for o in a.orders.split(",") for kk in a.keys.split(",")
-                                               for sc in a.scheds.split(",")]:
+                                               for sc in a.scheds.split(",") for pd in a.pdls.split(",")]:
             pj.lib().pjds_set_schedule(int(sch))
+            pm, pf = map(int, pdl.split(":"))
+            assert pj.lib().pjds_set_launch_overlap(pm, pf) == 0
             if fmt.startswith("pjds"):
                 if kspec == "none":
                     A.set_tile_keys(None)
@@ -81,12 +87,12 @@ for cfg in a.configs.split(","):
                 torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(a.reps): A.spmv(y, x)
+            for i in range(a.reps): A.spmv(ys[i % a.rotate], xs[i % a.rotate])
             e1.record()
             ck = clocks()  # after e1 is enqueued: a slow first NVML query must not delay e1 (it did: C2 +28 us)
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.reps * 1e-3
-            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sched": int(sch), "keys": kspec, "sigma": int(sg), "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
+            print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sched": int(sch), "keys": kspec, "sigma": int(sg), "pdl": pdl, "rotate": a.rotate, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
                               "stored_bytes": A.info.get("bytes_total"), "clk": ck}), flush=True)
           del A
