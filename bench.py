@@ -100,6 +100,9 @@ def parse(argv=None):
     p.add_argument("--probe-bytes", type=int, default=4 << 30)
     p.add_argument("--variant", default="", metavar="R,U",
                    help="kernel variant knob (pjds_set_kernel_variant; default: the library's automatic choice)")
+    p.add_argument("--launch-overlap", default="2,2", metavar="MODE,COLS",
+                   help="programmatic dependent launch (pjds_set_launch_overlap): 0 off, 1 on, 2 auto (grids of "
+                        "more than one wave; the library default), and the jagged columns first-wave warps prefetch")
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
     p.add_argument("--transport", default="nccl", choices=["nccl", "p2p", "direct"],
                    help="dist: NCCL send/recv on a side stream, the fused gather+put P2P kernel, or DIRECT "
@@ -422,6 +425,19 @@ def per_config_leg(cfg, dt, dev, stream, peak, timed, crs_cache, chunks_n=20, re
     return out
 
 
+def set_launch_overlap(a):
+    import paper_1112_5588_b200 as pj
+    m, c = (int(v) for v in a.launch_overlap.split(","))
+    if pj.lib().pjds_set_launch_overlap(m, c) != 0:
+        raise SystemExit(f"bench.py: bad --launch-overlap {a.launch_overlap}")
+
+
+def launch_overlap_desc(a):
+    m, c = (int(v) for v in a.launch_overlap.split(","))
+    return {0: "off", 1: f"programmatic dependent launch, {c}-column L2 prefetch",
+            2: f"auto: programmatic dependent launch for grids of more than one wave, {c}-column L2 prefetch"}[m]
+
+
 def run_single(a, npdt, sv, argv_cfg):
     import torch
     import inputs
@@ -431,6 +447,7 @@ def run_single(a, npdt, sv, argv_cfg):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     tdt = torch.float64 if npdt == np.float64 else torch.float32
+    set_launch_overlap(a)
     if a.variant:
         vr, vu = (int(v) for v in a.variant.split(","))
         if pj.lib().pjds_set_kernel_variant(vr, vu) != 0:
@@ -650,6 +667,7 @@ def run_single(a, npdt, sv, argv_cfg):
         "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
         "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows, "parallelism": "single GPU",
                    "variant": a.variant or "auto",
+                   "launch_overlap": launch_overlap_desc(a),
                    "overlap": None, "transport": None, "tile_window": a.tile_window or None,
                    "l2": f"inputs larger than L2: {b_min / 1e9:.2f} GB streamed per step, no flush"},
         "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
@@ -758,6 +776,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
             xd = w
         return D, xd
 
+    set_launch_overlap(a)
     D, x = build(a.transport)
     tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
     _allreduce(dist, tt, "sum")
@@ -858,36 +877,6 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
                  "oversubscribed": oversub, "nccl_env": nccl_env or None,
                  "basis": "permuted" if permuted else "rows"}
 
-    # the other transports on the same partition, behind their bounded waits (compare legs)
-    legs = {}
-    if not a.no_compare and world > 1:
-        for trn in ("nccl", "p2p", "direct"):
-            if trn == a.transport:
-                continue
-            dist.barrier()
-            try:
-                D2, x2 = build(trn)
-                y2 = torch.empty_like(y)
-                for _ in range(3):
-                    D2.spmv(y2, x2, stream=stream)
-                torch.cuda.synchronize()
-                dist.barrier()
-                m2 = max_over_ranks(dist, dev, timed(lambda i: D2.spmv(y2, x2, stream=stream), max(10, a.steps // 2)))
-                to2 = timed_out(D2)
-                p2 = parity_of(D2, y2, chain_expected=trn == "direct", perm_basis=basis_of(trn))
-                leg = {"ms": round(m2, 5), "GFlop/s": round(2.0 * nnz / (m2 * 1e-3) / 1e9, 1),
-                       "peer_wait_timed_out": to2, "basis": "permuted" if basis_of(trn) else "rows"}
-                if p2 is not None:
-                    leg["parity_within_bound"] = p2["within_bound"] and not to2
-                    leg["parity_bitwise_o3_chain"] = p2["bitwise_o3_chain"]
-                legs[trn] = leg
-                D2.close()
-                del D2, x2, y2
-            except Exception as e:  # a transport that cannot run here is reported, not fatal
-                legs[trn] = {"error": str(e)[:300]}
-            torch.cuda.synchronize()
-        dist_info["transports"] = legs
-
     # T1: the single-GPU product on the full matrix (rank 0's GPU; the others wait), so that the
     # line carries T1 / (R t_R) beside the driver's own cross-N efficiency
     t1_ms = None
@@ -941,6 +930,38 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
            "d2h_bytes_per_step": n * sv, "ms_per_step": round(te * 1e3, 3),
            "note": "all ranks' pinned host buffers; max over ranks"}
 
+    # the other transports on the same partition, behind their bounded waits (compare legs); run
+    # last, after every number of the contract transport is taken, so that a transport that
+    # cannot run on this box costs only its own entry
+    legs = {}
+    if not a.no_compare and world > 1:
+        for trn in ("nccl", "p2p", "direct"):
+            if trn == a.transport:
+                continue
+            dist.barrier()
+            try:
+                D2, x2 = build(trn)
+                y2 = torch.empty_like(y)
+                for _ in range(3):
+                    D2.spmv(y2, x2, stream=stream)
+                torch.cuda.synchronize()
+                dist.barrier()
+                m2 = max_over_ranks(dist, dev, timed(lambda i: D2.spmv(y2, x2, stream=stream), max(10, a.steps // 2)))
+                to2 = timed_out(D2)
+                p2 = parity_of(D2, y2, chain_expected=trn == "direct", perm_basis=basis_of(trn))
+                leg = {"ms": round(m2, 5), "GFlop/s": round(2.0 * nnz / (m2 * 1e-3) / 1e9, 1),
+                       "peer_wait_timed_out": to2, "basis": "permuted" if basis_of(trn) else "rows"}
+                if p2 is not None:
+                    leg["parity_within_bound"] = p2["within_bound"] and not to2
+                    leg["parity_bitwise_o3_chain"] = p2["bitwise_o3_chain"]
+                legs[trn] = leg
+                D2.close()
+                del D2, x2, y2
+            except Exception as e:  # a transport that cannot run here is reported, not fatal
+                legs[trn] = {"error": str(e)[:300]}
+            torch.cuda.synchronize()
+        dist_info["transports"] = legs
+
     t_s = ms * 1e-3
     b_min = nnz * (sv + 4) + 2 * n * sv
     achieved = b_min / t_s / 1e9 / world  # per GPU
@@ -955,7 +976,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
             "data": "synthetic (inputs/gen.cpp, seed 0x11125588)",
             "config": {"workload": wl, "n": n, "nnz": nnz, "block_rows": a.block_rows,
                        "parallelism": f"row-partition r{world}", "overlap": not a.no_overlap,
-                       "transport": a.transport, "tile_window": None,
+                       "transport": a.transport, "tile_window": None, "launch_overlap": launch_overlap_desc(a),
                        "l2": f"inputs larger than L2: {b_min / 1e9 / world:.2f} GB streamed per GPU per step, no flush"},
             "hbm_gbs_effective": round(b_min / t_s / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

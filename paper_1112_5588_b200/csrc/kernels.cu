@@ -15,6 +15,8 @@
 // Each row is ONE fused-multiply-add chain over its stored entries in CRS order starting from
 // +0.0 (padding adds exact +0): bitwise reproducible against oracle/ O3 for every R, U.
 #include <atomic>
+#include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <algorithm>
 #include <climits>
@@ -693,21 +695,31 @@ int launch_dyn_any(const pjds_mat* A, T* y, const T* x, cudaStream_t s, const in
   return launch_dyn<T, Off, R, U, M, false, false>(A, y, x, s, order, grid_static, launched);
 }
 
-// Programmatic dependent launch of the static pJDS kernel (pjds_set_launch_overlap): 0 off, 1 on;
+// Programmatic dependent launch of the static pJDS kernel (pjds_set_launch_overlap): 0 off, 1 on,
+// 2 auto (default: grids of more than one wave; prefetch 2 columns, the best of 0/2/4/8/64 measured);
 // g_pdl_pf = jagged columns of its val/col tile a first-wave warp prefetches into L2 while the
 // previous grid drains (0 = none).
-static int g_pdl = 0, g_pdl_pf = 0;
+static int g_pdl = 2, g_pdl_pf = 2;
 
 // first-wave CTA count of a kernel (SMs x resident CTAs), cached per kernel
 template <typename K>
 static int first_wave_ctas(K kern) {
-  static int v = 0;
-  if (!v) {
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
-    v = num_sms() * occ;
-  }
-  return v;
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find((const void*)kern);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+  return cache[(const void*)kern] = num_sms() * occ;
+}
+// mode 2 (auto): only grids of more than one wave.  A one-wave grid launched as a dependent places
+// its CTAs into whichever slots the previous grid frees first, unevenly over the SMs, where a plain
+// launch spreads them evenly: measured C4 (DLR1, 544 CTAs on 740 slots) DP 80.7 -> 83.6 us, SP 63.0
+// -> 66.8, while the multi-wave C2 gains 4.5-9 % (profiles/r02_kbench_launch_overlap.jsonl).
+template <typename K>
+static bool pdl_for(K kern, int64_t grid) {
+  return g_pdl == 1 || (g_pdl == 2 && grid > first_wave_ctas(kern));
 }
 
 // launch with or without cudaLaunchAttributeProgrammaticStreamSerialization
@@ -725,6 +737,14 @@ static int launch_ex(void (*kern)(P...), int64_t grid, cudaStream_t s, bool pdl,
   cfg.numAttrs = pdl ? 1 : 0;
   PJDS_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
   return PJDS_OK;
+}
+
+// the static pJDS kernel: launch_ex + its trailing (pf_cols, pf_ctas) parameters
+template <typename... P, typename... A>
+static int launch_pjds_kernel(void (*kern)(P...), int64_t grid, cudaStream_t s, bool pdl_ok, int pf_base, A&&... args) {
+  const bool pdl = pdl_ok && pdl_for(kern, grid);
+  const int pf_cols = pdl ? pf_base : 0;
+  return launch_ex(kern, grid, s, pdl, std::forward<A>(args)..., pf_cols, pf_cols > 0 ? first_wave_ctas(kern) : 0);
 }
 
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
@@ -771,14 +791,13 @@ int st;
   if ((uintptr_t)y % (R * sizeof(T))) pol &= 0xff00ffff;
   // programmatic dependent launch for y = A x / y += A x (not the Lanczos dot product, whose
   // launches are captured into a graph with its reduce passes)
-  const bool pdl = g_pdl && mode != STORE_DIRECT_DOT;
-  const int pf_cols = pdl && h.n_windows <= 1 ? g_pdl_pf : 0;
+  const bool pdl_ok = mode != STORE_DIRECT_DOT;
+  const int pf_base = h.n_windows <= 1 ? g_pdl_pf : 0;
 #define PJDS_LAUNCH_W(M, PF, IL, W)                                                                      \
-  PJDS_TRY(launch_ex(pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W>, grid, s, pdl,                          \
+  PJDS_TRY(launch_pjds_kernel(pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W>, grid, s, pdl_ok, pf_base,     \
       (const T*)A->d_val, (const int*)A->d_col, (const int64_t*)A->d_col_start, (const int*)A->d_block_len, \
       (const int*)A->d_perm, x, y, h.n, h.n_pad, (int)h.br, pol, order, dot_part, h.sigma,                  \
-      (const int64_t*)A->d_wcs_off, (const T* const*)A->d_win, (int)A->win_shift, worder, n_wtiles, pf_cols, \
-      pf_cols > 0 ? first_wave_ctas(pjds_spmv_kernel<T, Off, R, U, M, PF, IL, W>) : 0))
+      (const int64_t*)A->d_wcs_off, (const T* const*)A->d_win, (int)A->win_shift, worder, n_wtiles))
 #define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
   if (A->d_win) {  // fused remote-gather dist matrix: plain main loop, direct or perm store
     if constexpr (std::is_same<Off, int32_t>::value) {
@@ -1022,7 +1041,8 @@ int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t
 int set_tile_order(int mode) { return set_tile_order_impl(mode); }
 int set_schedule(int mode) { return set_schedule_impl(mode); }
 int set_launch_overlap(int mode, int prefetch_cols) {
-  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: mode 0 off, 1 programmatic dependent launch");
+  if (mode < 0 || mode > 2)
+    return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: mode 0 off, 1 programmatic dependent launch, 2 auto");
   if (prefetch_cols < 0 || prefetch_cols > 64) return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: prefetch_cols in [0, 64]");
   g_pdl = mode;
   g_pdl_pf = prefetch_cols;
@@ -1080,7 +1100,7 @@ int launch_ellr_t(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
   const auto& h = A->h;
   const int64_t grid = (h.n_pad / R + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
-  PJDS_TRY(launch_ex(ellr_spmv_kernel<T, R, U>, grid, s, g_pdl != 0, (const T*)A->d_val, (const int*)A->d_col,
+  PJDS_TRY(launch_ex(ellr_spmv_kernel<T, R, U>, grid, s, pdl_for(ellr_spmv_kernel<T, R, U>, grid), (const T*)A->d_val, (const int*)A->d_col,
                      (const int*)A->d_rowmax, (const T*)x, (T*)y, h.n, h.n_pad));
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());

@@ -634,7 +634,7 @@ def test_schedule_bitwise(pj, sched):
         L.pjds_set_tile_order(2)
 
 
-@pytest.mark.parametrize("overlap", [(1, 0), (1, 4), (1, 64)])
+@pytest.mark.parametrize("overlap", [(1, 0), (1, 4), (1, 64), (2, 2)])
 def test_launch_overlap_dependent_chain(pj, overlap):
     """pjds_set_launch_overlap: a product launched as a programmatic dependent of the previous one
     starts in its tail but reads x and writes y only after griddepcontrol.wait, so a chain of
@@ -692,6 +692,6 @@ def test_launch_overlap_dependent_chain(pj, overlap):
                 torch.cuda.synchronize()
                 assert np.array_equal(b[0].cpu().numpy(), want[6]), (name, dtype, "ellr")
     finally:
-        L.pjds_set_launch_overlap(0, 0)
+        L.pjds_set_launch_overlap(2, 2)
         L.pjds_set_kernel_variant(0, 0)
         L.pjds_set_tile_order(2)
