@@ -474,12 +474,13 @@ int pjds_set_schedule(int32_t mode);
    (griddepcontrol.wait) for that kernel to complete before reading x or writing y, so the stream
    order of an iterative scheme is kept.  prefetch_cols > 0: first-wave warps
    also prefetch the first prefetch_cols jagged columns of their val/col rows into L2 (global sort
-   only) before waiting.  mode 0: plain launches; mode 2 (default, prefetch_cols 2): mode 1 for
-   grids of more than one wave (SMs x resident CTAs), plain launches otherwise -- a one-wave grid
-   launched as a dependent lands unevenly on the SMs the previous grid frees first (measured slower
-   on the one-wave DLR1 matrix, faster on multi-wave ones).  The Lanczos-fused product always
-   launches plainly.  Errors: INVALID_ARG for mode outside {0, 1, 2} or prefetch_cols outside
-   [0, 64]. */
+   only) before waiting.  mode 3: dependent launch whose trigger is issued after a CTA's row chains
+   (the next grid is scheduled once every CTA has finished its chains; no prefetch).  mode 0: plain
+   launches; mode 2 (default, prefetch_cols 2): mode 1 for grids of more than one wave (SMs x
+   resident CTAs), mode 3 otherwise -- a one-wave grid launched as an early-triggered dependent
+   lands unevenly on the SMs the previous grid frees first (measured slower on the one-wave DLR1
+   matrix, faster on multi-wave ones).  The Lanczos-fused product always launches plainly.
+   Errors: INVALID_ARG for mode outside {0, 1, 2, 3} or prefetch_cols outside [0, 64]. */
 int pjds_set_launch_overlap(int32_t mode, int32_t prefetch_cols);
 
 /* Number of kernel launches this library has enqueued (process-wide counter). */

@@ -363,10 +363,11 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
                  double* __restrict__ dot_part, int64_t sigma, const int64_t* __restrict__ wcs_off,
                  const T* const* __restrict__ win, int win_shift, const int* __restrict__ warp_order,
-                 int64_t n_wtiles, int pf_cols, int pf_ctas) {
-  // programmatic dependent launch (see pdl_prologue): the next grid on the stream may be scheduled
-  // once every CTA of this one has started, i.e. into the SM slots this grid's last wave frees
-  pdl_trigger();
+                 int64_t n_wtiles, int pf_cols, int pf_ctas, int trig_late) {
+  // programmatic dependent launch (see pdl_trigger): the next grid on the stream may be scheduled
+  // once every CTA of this one has started, i.e. into the SM slots this grid's last wave frees --
+  // or, trig_late (one-wave grids), once every CTA has finished its row chains
+  if (!trig_late) pdl_trigger();
   __shared__ Off s_cs[kSmemCS];
   __shared__ const T* s_win[WIN ? kMaxWin : 1];
   if constexpr (WIN)
@@ -413,6 +414,7 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   const uint64_t pol_s = make_policy(pol & 0xff);
   const uint64_t pol_x = make_policy((pol >> 8) & 0xff);
   row_chains<T, Off, R, U, PIPE, IL, WIN>(acc, val, col, s_cs, col_start, k0, len, x, s_win, win_shift, pol_s, pol_x);
+  if (trig_late) pdl_trigger();
   const int y_kind = (pol >> 16) & 0xff;
   const int p_kind = (pol >> 24) & 0x7f;  // scattered stores through perm: 0 plain, 1 + L2 policy kind
   if ((MODE == STORE_DIRECT || MODE == STORE_DIRECT_DOT) && !IL && R > 1 && y_kind && k0 + R <= n) {
@@ -713,13 +715,19 @@ static int first_wave_ctas(K kern) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
   return cache[(const void*)kern] = num_sms() * occ;
 }
-// mode 2 (auto): only grids of more than one wave.  A one-wave grid launched as a dependent places
-// its CTAs into whichever slots the previous grid frees first, unevenly over the SMs, where a plain
-// launch spreads them evenly: measured C4 (DLR1, 544 CTAs on 740 slots) DP 80.7 -> 83.6 us, SP 63.0
-// -> 66.8, while the multi-wave C2 gains 4.5-9 % (profiles/r02_kbench_launch_overlap.jsonl).
+// mode 2 (auto): early trigger on grids of more than one wave, late trigger (after the row chains)
+// on one-wave grids.  A one-wave grid launched as an early-triggered dependent places its CTAs into
+// whichever slots the previous grid frees first, unevenly over the SMs, where a plain launch spreads
+// them evenly: measured C4 (DLR1, 544 CTAs on 740 slots) DP 80.7 -> 83.6 us, SP 63.0 -> 66.8; with
+// the late trigger 81.6 -> 79.2 and 63.2 -> 61.0; the multi-wave C2 gains 4.5-9 % either way
+// (profiles/r02_kbench_launch_overlap.jsonl, r02_kbench_launch_overlap_late.jsonl).
+// 0 plain launch, 1 dependent launch with the trigger at kernel start, 2 trigger after the chains
 template <typename K>
-static bool pdl_for(K kern, int64_t grid) {
-  return g_pdl == 1 || (g_pdl == 2 && grid > first_wave_ctas(kern));
+static int pdl_for(K kern, int64_t grid) {
+  if (g_pdl == 0) return 0;
+  if (g_pdl == 1) return 1;
+  if (g_pdl == 3) return 2;
+  return grid > first_wave_ctas(kern) ? 1 : 2;
 }
 
 // launch with or without cudaLaunchAttributeProgrammaticStreamSerialization
@@ -742,9 +750,10 @@ static int launch_ex(void (*kern)(P...), int64_t grid, cudaStream_t s, bool pdl,
 // the static pJDS kernel: launch_ex + its trailing (pf_cols, pf_ctas) parameters
 template <typename... P, typename... A>
 static int launch_pjds_kernel(void (*kern)(P...), int64_t grid, cudaStream_t s, bool pdl_ok, int pf_base, A&&... args) {
-  const bool pdl = pdl_ok && pdl_for(kern, grid);
-  const int pf_cols = pdl ? pf_base : 0;
-  return launch_ex(kern, grid, s, pdl, std::forward<A>(args)..., pf_cols, pf_cols > 0 ? first_wave_ctas(kern) : 0);
+  const int pdl = pdl_ok ? pdl_for(kern, grid) : 0;
+  const int pf_cols = pdl == 1 ? pf_base : 0;
+  return launch_ex(kern, grid, s, pdl != 0, std::forward<A>(args)..., pf_cols,
+                   pf_cols > 0 ? first_wave_ctas(kern) : 0, pdl == 2 ? 1 : 0);
 }
 
 static bool g_pipe = false;  // software-pipelined main loop (variant knob unroll + 16)
@@ -911,8 +920,8 @@ int launch_pjds_dt(const pjds_mat* A, void* y, const void* x, cudaStream_t s, in
 template <typename T, int R, int U>
 __global__ void __launch_bounds__(kThreads)
 ellr_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int* __restrict__ rowmax,
-                 const T* __restrict__ x, T* __restrict__ y, int64_t n, int64_t n_pad) {
-  pdl_trigger();  // programmatic dependent launch, as in the pJDS kernel (no prefetch)
+                 const T* __restrict__ x, T* __restrict__ y, int64_t n, int64_t n_pad, int trig_late) {
+  if (!trig_late) pdl_trigger();  // programmatic dependent launch, as in the pJDS kernel (no prefetch)
   const int64_t i0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * R;
   if (i0 >= n_pad) return;
   const uint64_t pol_s = policy_evict_first();
@@ -951,6 +960,7 @@ ellr_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
       for (int r = 0; r < R; ++r)
         if (j + u < lens.v[r]) acc[r] = fma_rn(v[u].v[r], xv[u][r], acc[r]);
   }
+  if (trig_late) pdl_trigger();
 #pragma unroll
   for (int r = 0; r < R; ++r)
     if (i0 + r < n) y[i0 + r] = acc[r];
@@ -1041,8 +1051,9 @@ int launch_pjds_spmv_dot(const pjds_mat* A, void* y, const void* x, cudaStream_t
 int set_tile_order(int mode) { return set_tile_order_impl(mode); }
 int set_schedule(int mode) { return set_schedule_impl(mode); }
 int set_launch_overlap(int mode, int prefetch_cols) {
-  if (mode < 0 || mode > 2)
-    return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: mode 0 off, 1 programmatic dependent launch, 2 auto");
+  if (mode < 0 || mode > 3)
+    return set_error(PJDS_ERR_INVALID_ARG,
+                     "launch overlap: mode 0 off, 1 dependent launch (early trigger), 2 auto, 3 dependent launch (late trigger)");
   if (prefetch_cols < 0 || prefetch_cols > 64) return set_error(PJDS_ERR_INVALID_ARG, "launch overlap: prefetch_cols in [0, 64]");
   g_pdl = mode;
   g_pdl_pf = prefetch_cols;
@@ -1100,8 +1111,9 @@ int launch_ellr_t(const ellr_mat* A, void* y, const void* x, cudaStream_t s) {
   const auto& h = A->h;
   const int64_t grid = (h.n_pad / R + kThreads - 1) / kThreads;
   if (grid == 0) return PJDS_OK;
-  PJDS_TRY(launch_ex(ellr_spmv_kernel<T, R, U>, grid, s, pdl_for(ellr_spmv_kernel<T, R, U>, grid), (const T*)A->d_val, (const int*)A->d_col,
-                     (const int*)A->d_rowmax, (const T*)x, (T*)y, h.n, h.n_pad));
+  const int pdl = pdl_for(ellr_spmv_kernel<T, R, U>, grid);
+  PJDS_TRY(launch_ex(ellr_spmv_kernel<T, R, U>, grid, s, pdl != 0, (const T*)A->d_val, (const int*)A->d_col,
+                     (const int*)A->d_rowmax, (const T*)x, (T*)y, h.n, h.n_pad, pdl == 2 ? 1 : 0));
   count_launch();
   PJDS_CUDA_TRY(cudaGetLastError());
   return PJDS_OK;

@@ -634,7 +634,7 @@ def test_schedule_bitwise(pj, sched):
         L.pjds_set_tile_order(2)
 
 
-@pytest.mark.parametrize("overlap", [(1, 0), (1, 4), (1, 64), (2, 2)])
+@pytest.mark.parametrize("overlap", [(1, 0), (1, 4), (1, 64), (2, 2), (3, 0)])
 def test_launch_overlap_dependent_chain(pj, overlap):
     """pjds_set_launch_overlap: a product launched as a programmatic dependent of the previous one
     starts in its tail but reads x and writes y only after griddepcontrol.wait, so a chain of

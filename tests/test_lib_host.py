@@ -235,7 +235,7 @@ def test_round2_knobs_and_collective_create_validation(pj):
     assert L.pjds_set_dist_nl_sigma(1024) == 0  # back to the default
     assert L.pjds_set_schedule(2) == -1 and L.pjds_set_schedule(0) == 0
     assert L.pjds_set_tile_order(4) == -1 and L.pjds_set_tile_order(2) == 0
-    assert L.pjds_set_launch_overlap(3, 0) == -1 and L.pjds_set_launch_overlap(-1, 0) == -1
+    assert L.pjds_set_launch_overlap(4, 0) == -1 and L.pjds_set_launch_overlap(-1, 0) == -1
     assert L.pjds_set_launch_overlap(1, 65) == -1 and L.pjds_set_launch_overlap(1, -1) == -1
     assert L.pjds_set_launch_overlap(1, 4) == 0 and L.pjds_set_launch_overlap(2, 2) == 0
     n = 64
