@@ -104,9 +104,11 @@ def parse(argv=None):
                    help="programmatic dependent launch (pjds_set_launch_overlap): 0 off, 1 on, 2 auto (grids of "
                         "more than one wave; the library default), and the jagged columns first-wave warps prefetch")
     p.add_argument("--dist", action="store_true", help="use the distributed path even at N=1 (one-rank NCCL group)")
-    p.add_argument("--transport", default="nccl", choices=["nccl", "p2p", "direct"],
-                   help="dist: NCCL send/recv on a side stream, the fused gather+put P2P kernel, or DIRECT "
-                        "(no exchange: one kernel whose nonlocal gathers read the owners' x windows)")
+    p.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p", "direct"],
+                   help="dist: NCCL send/recv on a side stream, the fused gather+put P2P kernel, DIRECT "
+                        "(no exchange: one kernel whose nonlocal gathers read the owners' x windows), or auto "
+                        "(default: each timed for 20 products on this partition, the fastest without a "
+                        "timed-out peer wait is the contract transport; the others are reported beside it)")
     p.add_argument("--nccl-env", action="append", default=[], metavar="KEY=VALUE",
                    help="NCCL tuning variable set before the communicator is created and recorded in the line "
                         "(e.g. NCCL_P2P_USE_CUDA_MEMCPY=1, NCCL_MAX_CTAS=4, NCCL_MAX_P2P_NCHANNELS=8); repeatable")
@@ -762,8 +764,6 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     def basis_of(transport):
         return a.basis == "permuted" or (a.basis == "auto" and transport == "direct")
 
-    permuted = basis_of(a.transport)
-
     def build(transport):
         D = pj.DistPjds.create(n, offs, rp, col, val, block_rows=a.block_rows, permuted=basis_of(transport),
                                transport=transport)
@@ -776,7 +776,42 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
             xd = w
         return D, xd
 
+    def timed_out(Dh):
+        t = torch.tensor([int(Dh.p2p_timed_out())], dtype=torch.int64, device=dev)
+        _allreduce(dist, t, "sum")
+        return int(t.item()) > 0
+
     set_launch_overlap(a)
+    stream = torch.cuda.current_stream()
+    timed = make_timer(stream)
+    selection = None
+    if a.transport == "auto":
+        # the library's three transports on this partition, 20 products each (max over ranks); the
+        # fastest one without a timed-out peer wait becomes the contract transport, the others are
+        # reported beside it (dist.transports) -- on NVSwitch the fused remote-gather kernel (DIRECT)
+        # is expected to win at large R, NCCL where remote loads cost more than the exchange
+        selection, best = {}, None
+        for trn in ("nccl", "p2p", "direct"):
+            dist.barrier()
+            try:
+                Ds, xs = build(trn)
+                ys = torch.empty(hi - lo, dtype=tdt, device=dev)
+                for _ in range(3):
+                    Ds.spmv(ys, xs, stream=stream)
+                torch.cuda.synchronize()
+                dist.barrier()
+                m = max_over_ranks(dist, dev, timed(lambda i: Ds.spmv(ys, xs, stream=stream), 20))
+                to = timed_out(Ds)
+                selection[trn] = {"ms": round(m, 5), "peer_wait_timed_out": to}
+                if not to and (best is None or m < best[1]):
+                    best = (trn, m)
+                Ds.close()
+                del Ds, xs, ys
+            except Exception as e:  # a transport that cannot run here is reported, not chosen
+                selection[trn] = {"error": str(e)[:300]}
+            torch.cuda.synchronize()
+        a.transport = best[0] if best else "nccl"
+    permuted = basis_of(a.transport)
     D, x = build(a.transport)
     tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
     _allreduce(dist, tt, "sum")
@@ -786,8 +821,6 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     probe_copy, probe_read = pj.bw_probe(a.probe_bytes, 5)
     peak_file = measured_peaks().get("hbm_gbs")
     peak = peak_file if peak_file else max(probe_copy, probe_read)
-    stream = torch.cuda.current_stream()
-    timed = make_timer(stream)
 
     def step(_i=0):
         D.spmv(y, x, stream=stream, no_overlap=a.no_overlap)
@@ -836,11 +869,6 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
         p["chunks"] = f"{len(chunks)} row ranges incl. every rank boundary"
         return p
 
-    def timed_out(Dh):
-        t = torch.tensor([int(Dh.p2p_timed_out())], dtype=torch.int64, device=dev)
-        _allreduce(dist, t, "sum")
-        return int(t.item()) > 0
-
     to_main = timed_out(D)
     # NCCL / P2P split the row into local + nonlocal chains (combined by one add, DESIGN reading 25):
     # not the unsplit O3 chain; DIRECT runs every row's whole chain in one kernel (bitwise expected)
@@ -866,7 +894,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     tp = phases["task"]
     comm = max(tp["exchange"], 1e-9)
     gain = ms_no / ms
-    dist_info = {"transport": a.transport, "ms_vector_mode": round(ms_no, 4), "speedup_task_over_vector": round(gain, 3),
+    dist_info = {"transport": a.transport, "transport_selection": selection, "ms_vector_mode": round(ms_no, 4), "speedup_task_over_vector": round(gain, 3),
                  # overlapping communication with computation gains at most 2x;
                  # not meaningful when ranks share a GPU (test mode: the stand-in NCCL serialises)
                  "m6_task_gain_le_2": None if oversub else bool(gain <= 2.0 + 1e-9),
