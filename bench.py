@@ -436,8 +436,10 @@ def set_launch_overlap(a):
 
 def launch_overlap_desc(a):
     m, c = (int(v) for v in a.launch_overlap.split(","))
-    return {0: "off", 1: f"programmatic dependent launch, {c}-column L2 prefetch",
-            2: f"auto: programmatic dependent launch for grids of more than one wave, {c}-column L2 prefetch"}[m]
+    return {0: "off", 1: f"programmatic dependent launch, early trigger, {c}-column L2 prefetch",
+            2: f"auto: programmatic dependent launch, early trigger + {c}-column L2 prefetch on grids of more "
+               "than one wave, trigger after the row chains on one-wave grids",
+            3: "programmatic dependent launch, trigger after the row chains"}[m]
 
 
 def run_single(a, npdt, sv, argv_cfg):
