@@ -778,6 +778,11 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
             xd = w
         return D, xd
 
+    t_start = time.perf_counter()
+
+    def progress(msg):  # stderr trace of the N > 1 phases (the JSON line stays alone on stdout)
+        print(f"bench.py[rank {rank}/{world}] {time.perf_counter() - t_start:8.1f}s {msg}", file=sys.stderr, flush=True)
+
     def timed_out(Dh):
         t = torch.tensor([int(Dh.p2p_timed_out())], dtype=torch.int64, device=dev)
         _allreduce(dist, t, "sum")
@@ -787,6 +792,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     stream = torch.cuda.current_stream()
     timed = make_timer(stream)
     selection = None
+    built = {}  # transport -> (handle, x) created once per run (communicators are not re-created)
     if a.transport == "auto":
         # the library's three transports on this partition, 20 products each (max over ranks); the
         # fastest one without a timed-out peer wait becomes the contract transport, the others are
@@ -795,6 +801,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
         selection, best = {}, None
         for trn in ("nccl", "p2p", "direct"):
             dist.barrier()
+            progress(f"transport selection: {trn}")
             try:
                 Ds, xs = build(trn)
                 ys = torch.empty(hi - lo, dtype=tdt, device=dev)
@@ -807,14 +814,15 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
                 selection[trn] = {"ms": round(m, 5), "peer_wait_timed_out": to}
                 if not to and (best is None or m < best[1]):
                     best = (trn, m)
-                Ds.close()
-                del Ds, xs, ys
+                built[trn] = (Ds, xs)  # kept: the contract transport and the legs reuse them
+                del ys
             except Exception as e:  # a transport that cannot run here is reported, not chosen
                 selection[trn] = {"error": str(e)[:300]}
             torch.cuda.synchronize()
         a.transport = best[0] if best else "nccl"
+        progress(f"transport selection: {selection} -> {a.transport}")
     permuted = basis_of(a.transport)
-    D, x = build(a.transport)
+    D, x = built.pop(a.transport) if a.transport in built else build(a.transport)
     tt = torch.tensor([nnz_loc], dtype=torch.int64, device=dev)
     _allreduce(dist, tt, "sum")
     nnz = int(tt.item())
@@ -839,6 +847,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
     dist.barrier()
     torch.cuda.synchronize()
     ms = max_over_ranks(dist, dev, ms)
+    progress(f"timed {a.steps} steps of {a.transport}: {ms:.4f} ms")
     lt = torch.tensor([launches], dtype=torch.int64, device=dev)
     _allreduce(dist, lt, "sum")
     launches = int(lt.item())
@@ -871,6 +880,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
         p["chunks"] = f"{len(chunks)} row ranges incl. every rank boundary"
         return p
 
+    progress("trials done; parity")
     to_main = timed_out(D)
     # NCCL / P2P split the row into local + nonlocal chains (combined by one add, DESIGN reading 25):
     # not the unsplit O3 chain; DIRECT runs every row's whole chain in one kernel (bitwise expected)
@@ -907,6 +917,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
                  "oversubscribed": oversub, "nccl_env": nccl_env or None,
                  "basis": "permuted" if permuted else "rows"}
 
+    progress("vector mode and phases done")
     # T1: the single-GPU product on the full matrix (rank 0's GPU; the others wait), so that the
     # line carries T1 / (R t_R) beside the driver's own cross-N efficiency
     t1_ms = None
@@ -952,6 +963,7 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
             D.spmv(yd, xdst if a.transport == "direct" else xd, stream=stream, no_overlap=a.no_overlap)
         yh.copy_(yd, non_blocking=True)
 
+    progress("T1 done; e2e")
     e2e_step()
     torch.cuda.synchronize()
     dist.barrier()
@@ -969,8 +981,9 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
             if trn == a.transport:
                 continue
             dist.barrier()
+            progress(f"compare leg: {trn}")
             try:
-                D2, x2 = build(trn)
+                D2, x2 = built.pop(trn) if trn in built else build(trn)
                 y2 = torch.empty_like(y)
                 for _ in range(3):
                     D2.spmv(y2, x2, stream=stream)
@@ -991,6 +1004,9 @@ def run_dist(a, world, rank, local_rank, npdt, sv):
                 legs[trn] = {"error": str(e)[:300]}
             torch.cuda.synchronize()
         dist_info["transports"] = legs
+    for Dk, _ in built.values():  # selection handles no leg used (--no-compare)
+        Dk.close()
+    built.clear()
 
     t_s = ms * 1e-3
     b_min = nnz * (sv + 4) + 2 * n * sv

@@ -1,4 +1,4 @@
-# round 2, call 32: L2 set-aside for evict_last x lines at intermediate sizes (C5, default order)
+# round 2, call 35: bench --transport auto reusing the selection handles (no communicator re-creation)
 set -x
-timeout 900 python tools/l2_persist_probe.py --keys none --limits 0,8388608,16777216,25165824,33554432,50331648,67108864,max,0 --reps 40 > gpurun_out/r02c32_persist.jsonl 2> gpurun_out/r02c32_persist.err
-timeout 900 python tools/l2_persist_probe.py --dtype f32 --keys none --limits 0,16777216,33554432,max,0 --reps 40 >> gpurun_out/r02c32_persist.jsonl 2>> gpurun_out/r02c32_persist.err
+timeout 1200 python -m pytest tests/test_gpu_bench_dist.py -x -q > gpurun_out/r02c35_bench_dist.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c35_bench_dist.txt
+timeout 900 python bench.py --gpus 4 --oversubscribe --config C5 --steps 10 --warmup 3 --e2e-steps 2 > gpurun_out/r02c35_bench_c5_r4_auto.json 2> gpurun_out/r02c35_bench_c5_r4_auto.err; echo "rc=$?" >> gpurun_out/r02c35_bench_c5_r4_auto.err
