@@ -147,6 +147,7 @@ typedef struct {
   int64_t sigma;          /* sort scope in rows (n_pad for the paper's global sort) */
   int64_t n_windows;      /* number of sort windows (1 for the global sort) */
   int64_t col_start_len;  /* entries of the concatenated per-window col_start (width+1 if global) */
+  int32_t col_compressible; /* 1: col lives in generic compressible memory (pjds_set_compression) */
 } pjds_info_t;
 
 int pjds_info(pjds_t A, pjds_info_t* out);
@@ -209,6 +210,7 @@ typedef struct {
   int64_t useful_fma, padded_fma, idle_lane_slots; /* idle = sum_warps sum_lanes (max - len) */
   int64_t bytes_values, bytes_indices, bytes_aux, bytes_total; /* aux = rowmax int32[n_pad] */
   int32_t on_device, device;
+  int32_t col_compressible; /* 1: col lives in generic compressible memory (pjds_set_compression) */
 } ellr_info_t;
 int ellr_info(ellr_t A, ellr_info_t* out);
 int ellr_footprint(ellr_t A, pjds_footprint_t* out); /* see pjds_footprint */
@@ -482,6 +484,15 @@ int pjds_set_schedule(int32_t mode);
    matrix, faster on multi-wave ones).  The Lanczos-fused product always launches plainly.
    Errors: INVALID_ARG for mode outside {0, 1, 2, 3} or prefetch_cols outside [0, 64]. */
 int pjds_set_launch_overlap(int32_t mode, int32_t prefetch_cols);
+/* pjds_set_compression (process-wide knob, applied when a handle uploads; results are identical):
+   mode 1 (default): the int32 column-index array of every pJDS / ELLPACK-R handle (>= 1 MiB) is
+   placed in generic compressible device memory (driver VMM, CU_MEM_ALLOCATION_COMP_GENERIC), where
+   B200 compresses data between L2 and HBM transparently to the kernels -- the format, layout and
+   values are those of PAPER.md L213-237 bit for bit, only the bytes crossing the HBM interface
+   shrink (column indices of a jagged column are runs of nearby integers).  Falls back to plain
+   cudaMalloc when the driver does not grant compression; pjds_info / ellr_info report
+   col_compressible.  mode 0: plain cudaMalloc.  Errors: INVALID_ARG for mode outside {0, 1}. */
+int pjds_set_compression(int32_t mode);
 
 /* Number of kernel launches this library has enqueued (process-wide counter). */
 int64_t pjds_launch_count(void);

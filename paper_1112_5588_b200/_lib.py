@@ -25,14 +25,14 @@ class PjdsInfo(ctypes.Structure):
                 ("useful_fma", c_i64), ("padded_fma", c_i64), ("idle_lane_slots", c_i64),
                 ("bytes_values", c_i64), ("bytes_indices", c_i64), ("bytes_aux", c_i64), ("bytes_total", c_i64),
                 ("data_reduction_vs_ellpack", c_dbl), ("on_device", c_i32), ("device", c_i32),
-                ("sigma", c_i64), ("n_windows", c_i64), ("col_start_len", c_i64)]
+                ("sigma", c_i64), ("n_windows", c_i64), ("col_start_len", c_i64), ("col_compressible", c_i32)]
 
 
 class EllrInfo(ctypes.Structure):
     _fields_ = [("n", c_i64), ("nnz", c_i64), ("n_pad", c_i64), ("stored", c_i64), ("width", c_i32), ("dtype", c_i32),
                 ("useful_fma", c_i64), ("padded_fma", c_i64), ("idle_lane_slots", c_i64),
                 ("bytes_values", c_i64), ("bytes_indices", c_i64), ("bytes_aux", c_i64), ("bytes_total", c_i64),
-                ("on_device", c_i32), ("device", c_i32)]
+                ("on_device", c_i32), ("device", c_i32), ("col_compressible", c_i32)]
 
 
 class Footprint(ctypes.Structure):
@@ -115,6 +115,7 @@ _SIGS = {
     "pjds_set_tile_order": [c_i32],
     "pjds_set_schedule": [c_i32],
     "pjds_set_launch_overlap": [c_i32, c_i32],
+    "pjds_set_compression": [c_i32],
     "pjds_set_tile_keys": [c_p, c_p, c_i64],
     "pjds_lanczos": [c_p, c_p, c_i32, c_p, c_p, c_p, c_p],
     "pjds_tridiag_eigenvalues": [c_i32, c_p, c_p, c_p],

@@ -24,7 +24,7 @@ static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
 }
 
 int free_pjds_device(pjds_mat* A) {
-  cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
+  cudaFree(A->d_val); dev_free(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
   cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off); cudaFree(A->d_sched);
   A->d_wcs_off = nullptr;
   A->d_sched = nullptr;
@@ -80,7 +80,7 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
   std::vector<int64_t> woff = windowed ? h.wcs_off : std::vector<int64_t>{0, (int64_t)cs_abs.size()};
   int s = PJDS_OK;
   if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
-      (s = dmalloc_copy(&A->d_col, h.col.data(), h.col.size() * 4)) ||
+      (s = dalloc_index(&A->d_col, h.col.data(), h.col.size() * 4)) ||
       (s = dmalloc_copy(&A->d_col_start, cs_abs.data(), cs_abs.size() * 8)) ||
       (s = dmalloc_copy(&A->d_wcs_off, woff.data(), woff.size() * 8)) ||
       (s = dmalloc_copy(&A->d_block_len, h.block_len.data(), h.block_len.size() * 4)) ||
@@ -319,6 +319,7 @@ int pjds_info(pjds_t A, pjds_info_t* o) {
   o->sigma = h.sigma;
   o->n_windows = h.n_windows;
   o->col_start_len = (int64_t)h.col_start.size();
+  o->col_compressible = A->on_device && is_compressible(A->d_col);
   return PJDS_OK;
 }
 
@@ -367,9 +368,9 @@ int ellr_create_from_crs(ellr_t* out, int64_t n, const int64_t* rowptr, const in
     auto& h = A->h;
     cudaGetDevice(&A->device);
     if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
-        (s = dmalloc_copy(&A->d_col, h.col.data(), h.col.size() * 4)) ||
+        (s = dalloc_index(&A->d_col, h.col.data(), h.col.size() * 4)) ||
         (s = dmalloc_copy(&A->d_rowmax, h.rowmax.data(), h.rowmax.size() * 4))) {
-      cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_rowmax);
+      cudaFree(A->d_val); dev_free(A->d_col); cudaFree(A->d_rowmax);
     } else {
       A->on_device = true;
       std::vector<int32_t>().swap(h.col);
@@ -388,7 +389,7 @@ int ellr_destroy(ellr_t A) {
   if (!A) return PJDS_OK;
   if (A->on_device) {
     DeviceGuard dg(A->device);
-    cudaFree(A->d_val); cudaFree(A->d_col); cudaFree(A->d_rowmax);
+    cudaFree(A->d_val); dev_free(A->d_col); cudaFree(A->d_rowmax);
   }
   delete A;
   return PJDS_OK;
@@ -414,6 +415,7 @@ int ellr_info(ellr_t A, ellr_info_t* o) {
   o->bytes_total = o->bytes_values + o->bytes_indices + o->bytes_aux;
   o->on_device = A->on_device;
   o->device = A->device;
+  o->col_compressible = A->on_device && is_compressible(A->d_col);
   return PJDS_OK;
 }
 
@@ -485,6 +487,7 @@ int pjds_set_y_store(pjds_t A, int32_t kind) {
 int pjds_set_tile_order(int32_t mode) { return set_tile_order(mode); }
 int pjds_set_schedule(int32_t mode) { return set_schedule(mode); }
 int pjds_set_launch_overlap(int32_t mode, int32_t prefetch_cols) { return set_launch_overlap(mode, prefetch_cols); }
+int pjds_set_compression(int32_t mode) { return set_compression(mode); }
 
 int pjds_set_tile_keys(pjds_t A, const int64_t* key, int64_t n) {
   if (!A) return set_error(PJDS_ERR_INVALID_ARG, "pjds_set_tile_keys: NULL handle");

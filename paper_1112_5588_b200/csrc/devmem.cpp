@@ -1,0 +1,181 @@
+// Device allocations of the matrix's column-index streams in generic compressible memory.
+//
+// B200 compresses data between L2 and HBM for allocations created with
+// CU_MEM_ALLOCATION_COMP_GENERIC (driver VMM API), transparently to every load and store: the
+// pJDS / ELLPACK-R arrays keep their layout and contents bit for bit (Listing 2;
+// readings 5 and 7), only the number of bytes that cross the HBM interface changes.  The jagged
+// int32 column indices of the HMEp / sAMG / DLR1 shapes are runs of nearby integers and compress
+// (C3 permuted basis: 2.09x fewer DRAM bytes on a read of the array, profiles/r02_compress_probe.txt);
+// the FP values and x (uniform random) do not, so only col goes there.
+//
+// The driver entry points come from cudaGetDriverEntryPoint (no link-time libcuda dependency: the
+// library still loads on a GPU-less host).  Data is staged with a plain cudaMalloc + H2D copy and
+// moved into the compressible allocation by an SM copy kernel (L2 compresses what SMs write back).
+// Any failure (no driver support, no compression granted, out of memory) falls back to cudaMalloc.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace pjds {
+namespace {
+
+struct Driver {
+  bool ok = false;
+  CUresult (*getGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*getProps)(CUmemAllocationProp*, CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*addressFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+};
+
+template <typename F>
+bool entry(const char* name, F* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) {
+    cudaGetLastError();
+    return false;
+  }
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    d.ok = entry("cuMemGetAllocationGranularity", &d.getGranularity) && entry("cuMemCreate", &d.create) &&
+           entry("cuMemGetAllocationPropertiesFromHandle", &d.getProps) && entry("cuMemAddressReserve", &d.reserve) &&
+           entry("cuMemMap", &d.map) && entry("cuMemSetAccess", &d.setAccess) && entry("cuMemUnmap", &d.unmap) &&
+           entry("cuMemAddressFree", &d.addressFree) && entry("cuMemRelease", &d.release);
+  });
+  return d;
+}
+
+struct Vmm {
+  CUmemGenericAllocationHandle handle;
+  size_t size;
+};
+std::mutex g_mu;
+std::unordered_map<void*, Vmm> g_vmm;  // compressible allocations by base pointer
+int g_compress = 1;                      // pjds_set_compression (process-wide; applies at upload)
+
+// A compressible allocation of >= bytes on `device`; false (nothing allocated) if the driver does not
+// grant generic compression for it.
+bool vmm_alloc(void** out, size_t bytes, int device) {
+  Driver& d = driver();
+  if (!d.ok) return false;
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.allocFlags.compressionType = CU_MEM_ALLOCATION_COMP_GENERIC;
+  size_t gran = 0;
+  if (d.getGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran) return false;
+  const size_t size = (bytes + gran - 1) / gran * gran;
+  CUmemGenericAllocationHandle h;
+  if (d.create(&h, size, &prop, 0) != CUDA_SUCCESS) return false;
+  CUmemAllocationProp got = {};
+  if (d.getProps(&got, h) != CUDA_SUCCESS || got.allocFlags.compressionType != CU_MEM_ALLOCATION_COMP_GENERIC) {
+    d.release(h);
+    return false;
+  }
+  CUdeviceptr p = 0;
+  if (d.reserve(&p, size, gran, 0, 0) != CUDA_SUCCESS) {
+    d.release(h);
+    return false;
+  }
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.map(p, size, 0, h, 0) != CUDA_SUCCESS) {
+    d.addressFree(p, size);
+    d.release(h);
+    return false;
+  }
+  if (d.setAccess(p, size, &acc, 1) != CUDA_SUCCESS) {
+    d.unmap(p, size);
+    d.addressFree(p, size);
+    d.release(h);
+    return false;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_vmm[(void*)p] = {h, size};
+  *out = (void*)p;
+  return true;
+}
+
+}  // namespace
+
+int set_compression(int mode) {
+  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "compression: 0 off, 1 generic compressible memory for col");
+  g_compress = mode;
+  return PJDS_OK;
+}
+
+bool is_compressible(const void* p) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_vmm.count(const_cast<void*>(p)) != 0;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  Vmm v{};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_vmm.find(p);
+    if (it == g_vmm.end()) {
+      cudaFree(p);
+      return;
+    }
+    v = it->second;
+    g_vmm.erase(it);
+  }
+  Driver& d = driver();
+  cudaDeviceSynchronize();  // no kernel of this process may still read the range
+  d.unmap((CUdeviceptr)p, v.size);
+  d.addressFree((CUdeviceptr)p, v.size);
+  d.release(v.handle);
+}
+
+// Column indices (int32) of `bytes` from the host: compressible memory when enabled and granted,
+// else plain device memory.  Empty arrays get a 16-byte zeroed plain allocation.
+int dalloc_index(int32_t** dst, const int32_t* src, size_t bytes) {
+  *dst = nullptr;
+  int device = 0;
+  PJDS_CUDA_TRY(cudaGetDevice(&device));
+  void* p = nullptr;
+  if (g_compress && bytes >= (size_t(1) << 20) && vmm_alloc(&p, bytes, device)) {
+    void* stage = nullptr;
+    const size_t sb = (bytes + 15) & ~size_t(15);
+    cudaError_t e = cudaMalloc(&stage, sb);
+    if (e == cudaSuccess) e = cudaMemcpy(stage, src, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      const int s = launch_copy16(stage, p, sb, 0);
+      e = s == PJDS_OK ? cudaDeviceSynchronize() : cudaErrorLaunchFailure;
+    }
+    cudaFree(stage);
+    if (e == cudaSuccess) {
+      *dst = (int32_t*)p;
+      return PJDS_OK;
+    }
+    cudaGetLastError();
+    dev_free(p);
+    return set_error(PJDS_ERR_CUDA, std::string("compressible column-index upload: ") + cudaGetErrorString(e));
+  }
+  PJDS_CUDA_TRY(cudaMalloc((void**)dst, bytes ? bytes : 16));
+  if (!bytes) PJDS_CUDA_TRY(cudaMemset(*dst, 0, 16));
+  if (src && bytes) PJDS_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return PJDS_OK;
+}
+
+}  // namespace pjds

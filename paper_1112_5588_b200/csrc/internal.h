@@ -150,5 +150,11 @@ int set_tile_order(int mode);
 int set_schedule(int mode);
 int set_launch_overlap(int mode, int prefetch_cols);
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs);
+int launch_copy16(const void* src, void* dst, size_t bytes, cudaStream_t s);  // bytes % 16 == 0
+// devmem.cpp: column indices in generic compressible memory (pjds_set_compression)
+int set_compression(int mode);
+int dalloc_index(int32_t** dst, const int32_t* src, size_t bytes);
+void dev_free(void* p);  // cudaFree, or the VMM release of a compressible allocation
+bool is_compressible(const void* p);
 void count_launch(int64_t k = 1);
 }  // namespace pjds

@@ -1164,6 +1164,16 @@ int launch_pack(const int32_t* idx, int64_t count, const void* x, void* buf, int
   return PJDS_OK;
 }
 
+int launch_copy16(const void* src, void* dst, size_t bytes, cudaStream_t s) {
+  const int64_t n = (int64_t)(bytes / 16);
+  if (!n) return PJDS_OK;
+  const int64_t grid = std::min<int64_t>((n + kThreads - 1) / kThreads, int64_t(148) * 16);
+  copy_kernel<<<(unsigned)grid, kThreads, 0, s>>>((const int4*)src, (int4*)dst, n);
+  count_launch();
+  PJDS_CUDA_TRY(cudaGetLastError());
+  return PJDS_OK;
+}
+
 int bw_probe(int64_t bytes, int reps, double* copy_gbs, double* read_gbs) {
   if (bytes < (1 << 20) || reps < 1) return set_error(PJDS_ERR_INVALID_ARG, "bw_probe: bytes >= 1 MiB, reps >= 1");
   int64_t n = bytes / 16;

@@ -695,3 +695,41 @@ def test_launch_overlap_dependent_chain(pj, overlap):
         L.pjds_set_launch_overlap(2, 2)
         L.pjds_set_kernel_variant(0, 0)
         L.pjds_set_tile_order(2)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_compressible_col_bitwise(pj, name):
+    """pjds_set_compression: the column indices in generic compressible memory are the same array
+    (device export == the oracle converter's), the product is bitwise the same as with plain memory
+    and the FMA chain, for pJDS (both bases) and ELLPACK-R; info reports where col lives."""
+    L = pj.lib()
+    try:
+        for dtype in (np.float64, np.float32):
+            n, rp, col, val = inputs.config_crs(name, dtype=dtype)
+            x = inputs.vector(n, dtype)
+            xt = tdev(x)
+            chain = oracle.spmv_chain(n, rp, col, val, x)
+            ref = convert.pjds_reference(n, rp, col, val, 128, symmetric=True)
+            for mode in (0, 1):
+                assert L.pjds_set_compression(mode) == 0
+                for sym in (False, True):
+                    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=128, symmetric=sym)
+                    assert A.info["col_compressible"] == mode, (name, mode, A.info["col_compressible"])
+                    if sym:
+                        assert np.array_equal(A.export()["col"], np.asarray(ref["col"], np.int32))
+                    xin = A.to_permuted(torch.empty_like(xt), xt) if sym else xt
+                    y = torch.full_like(xt, float("nan"))
+                    A.spmv(y, xin)
+                    yo = A.from_permuted(torch.empty_like(y), y) if sym else y
+                    torch.cuda.synchronize()
+                    assert np.array_equal(yo.cpu().numpy(), chain), (name, dtype, mode, sym)
+                    del A
+                E = pj.EllrMatrix.from_crs(n, rp, col, val)
+                assert E.info["col_compressible"] == mode
+                y = torch.full_like(xt, float("nan"))
+                E.spmv(y, xt)
+                torch.cuda.synchronize()
+                assert np.array_equal(y.cpu().numpy(), chain), (name, dtype, mode, "ellr")
+                del E
+    finally:
+        L.pjds_set_compression(1)

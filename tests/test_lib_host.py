@@ -238,6 +238,8 @@ def test_round2_knobs_and_collective_create_validation(pj):
     assert L.pjds_set_launch_overlap(4, 0) == -1 and L.pjds_set_launch_overlap(-1, 0) == -1
     assert L.pjds_set_launch_overlap(1, 65) == -1 and L.pjds_set_launch_overlap(1, -1) == -1
     assert L.pjds_set_launch_overlap(1, 4) == 0 and L.pjds_set_launch_overlap(2, 2) == 0
+    assert L.pjds_set_compression(2) == -1 and L.pjds_set_compression(-1) == -1
+    assert L.pjds_set_compression(0) == 0 and L.pjds_set_compression(1) == 0
     n = 64
     _, rp, col, val = inputs.small("random", n, seed=2, max=9)
     A = pj.PjdsMatrix.from_crs(n, rp, col, val, host_only=True)

@@ -36,8 +36,10 @@ SEG = {"C1": 1024, "C3": 15504, "C5": 142506}
 p.add_argument("--once", action="store_true", help="single launch per variant (for ncu)")
 p.add_argument("--pdls", default="0:0", help="launch overlap mode:prefetch_cols list (pjds_set_launch_overlap)")
 p.add_argument("--rotate", type=int, default=1, help="x/y pairs cycled over the timed launches (L2 carry-over)")
+p.add_argument("--compress", type=int, default=1, help="pjds_set_compression mode for the handles built")
 a = p.parse_args()
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6553.3
+assert pj.lib().pjds_set_compression(a.compress) == 0
 pj.bw_probe(1 << 30, 20)  # bring the GPU out of its idle clocks before the first measurement
 for cfg in a.configs.split(","):
     for dts in a.dtypes.split(","):
@@ -94,6 +96,6 @@ for cfg in a.configs.split(","):
             t = e0.elapsed_time(e1) / a.reps * 1e-3
             print(json.dumps({"cfg": cfg, "dtype": dts, "fmt": fmt, "var": var, "pol": polk, "order": order, "sched": int(sch), "keys": kspec, "sigma": int(sg), "pdl": pdl, "rotate": a.rotate, "us": round(t * 1e6, 1), "gflops": round(2 * nnz / t / 1e9, 1),
                               "eff_gbs": round(bmin / t / 1e9, 1), "frac": round(bmin / t / 1e9 / peak, 3),
-                              "stored_bytes": A.info.get("bytes_total"), "clk": ck}), flush=True)
+                              "stored_bytes": A.info.get("bytes_total"), "col_compressible": A.info.get("col_compressible"), "clk": ck}), flush=True)
           del A
         del rp, col, val
