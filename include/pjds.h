@@ -485,8 +485,8 @@ int pjds_set_schedule(int32_t mode);
    Errors: INVALID_ARG for mode outside {0, 1, 2, 3} or prefetch_cols outside [0, 64]. */
 int pjds_set_launch_overlap(int32_t mode, int32_t prefetch_cols);
 /* pjds_set_compression (process-wide knob, applied when a handle uploads; results are identical):
-   mode 1 (default): the int32 column-index array of every pJDS / ELLPACK-R handle (>= 1 MiB) is
-   placed in generic compressible device memory (driver VMM, CU_MEM_ALLOCATION_COMP_GENERIC), where
+   mode 1 (default): the int32 index arrays of every pJDS / ELLPACK-R handle (>= 1 MiB: col, the
+   pJDS row-store targets perm, the ELLPACK-R rowmax) are placed in generic compressible device memory (driver VMM, CU_MEM_ALLOCATION_COMP_GENERIC), where
    B200 compresses data between L2 and HBM transparently to the kernels -- the format, layout and
    values are those of PAPER.md L213-237 bit for bit, only the bytes crossing the HBM interface
    shrink (column indices of a jagged column are runs of nearby integers).  Falls back to plain

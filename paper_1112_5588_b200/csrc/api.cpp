@@ -25,7 +25,7 @@ static int dmalloc_copy(P** dst, const void* src, size_t bytes) {
 
 int free_pjds_device(pjds_mat* A) {
   cudaFree(A->d_val); dev_free(A->d_col); cudaFree(A->d_col_start); cudaFree(A->d_block_len);
-  cudaFree(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off); cudaFree(A->d_sched);
+  dev_free(A->d_perm); cudaFree(A->d_xs); cudaFree(A->d_ys); cudaFree(A->d_wcs_off); cudaFree(A->d_sched);
   A->d_wcs_off = nullptr;
   A->d_sched = nullptr;
   for (int b = 0; b < 2; ++b) {
@@ -84,7 +84,7 @@ int upload_pjds(pjds_mat* A, const int32_t* store_map) {
       (s = dmalloc_copy(&A->d_col_start, cs_abs.data(), cs_abs.size() * 8)) ||
       (s = dmalloc_copy(&A->d_wcs_off, woff.data(), woff.size() * 8)) ||
       (s = dmalloc_copy(&A->d_block_len, h.block_len.data(), h.block_len.size() * 4)) ||
-      (s = dmalloc_copy(&A->d_perm, tp, (size_t)h.n * 4)) ||
+      (s = dalloc_index(&A->d_perm, tp, (size_t)h.n * 4)) ||
       (s = dmalloc_copy(&A->d_sched, nullptr, 0))) {  // 16 zeroed bytes: the dynamic-schedule counters
     free_pjds_device(A);
     return s;
@@ -369,8 +369,8 @@ int ellr_create_from_crs(ellr_t* out, int64_t n, const int64_t* rowptr, const in
     cudaGetDevice(&A->device);
     if ((s = dmalloc_copy(&A->d_val, h.val.data(), h.val.size())) ||
         (s = dalloc_index(&A->d_col, h.col.data(), h.col.size() * 4)) ||
-        (s = dmalloc_copy(&A->d_rowmax, h.rowmax.data(), h.rowmax.size() * 4))) {
-      cudaFree(A->d_val); dev_free(A->d_col); cudaFree(A->d_rowmax);
+        (s = dalloc_index(&A->d_rowmax, h.rowmax.data(), h.rowmax.size() * 4))) {
+      cudaFree(A->d_val); dev_free(A->d_col); dev_free(A->d_rowmax);
     } else {
       A->on_device = true;
       std::vector<int32_t>().swap(h.col);
@@ -389,7 +389,7 @@ int ellr_destroy(ellr_t A) {
   if (!A) return PJDS_OK;
   if (A->on_device) {
     DeviceGuard dg(A->device);
-    cudaFree(A->d_val); dev_free(A->d_col); cudaFree(A->d_rowmax);
+    cudaFree(A->d_val); dev_free(A->d_col); dev_free(A->d_rowmax);
   }
   delete A;
   return PJDS_OK;

@@ -1,12 +1,14 @@
-// Device allocations of the matrix's column-index streams in generic compressible memory.
+// Device allocations of the matrix's int32 index streams (column indices; the row-store targets
+// perm of pJDS and the row lengths rowmax of ELLPACK-R) in generic compressible memory.
 //
 // B200 compresses data between L2 and HBM for allocations created with
 // CU_MEM_ALLOCATION_COMP_GENERIC (driver VMM API), transparently to every load and store: the
 // pJDS / ELLPACK-R arrays keep their layout and contents bit for bit (Listing 2;
 // readings 5 and 7), only the number of bytes that cross the HBM interface changes.  The jagged
 // int32 column indices of the HMEp / sAMG / DLR1 shapes are runs of nearby integers and compress
-// (C3 permuted basis: 2.09x fewer DRAM bytes on a read of the array, profiles/r02_compress_probe.txt);
-// the FP values and x (uniform random) do not, so only col goes there.
+// (C3 permuted basis: 2.09x fewer DRAM bytes on a read of the array, profiles/r02_compress_probe.txt),
+// and so do perm (ascending within each length class) and rowmax (small values); the FP values and
+// x (uniform random) do not, so only the int32 index arrays go there.
 //
 // The driver entry points come from cudaGetDriverEntryPoint (no link-time libcuda dependency: the
 // library still loads on a GPU-less host).  Data is staged with a plain cudaMalloc + H2D copy and
@@ -147,7 +149,7 @@ void dev_free(void* p) {
   d.release(v.handle);
 }
 
-// Column indices (int32) of `bytes` from the host: compressible memory when enabled and granted,
+// An int32 index array of `bytes` from the host: compressible memory when enabled and granted,
 // else plain device memory.  Empty arrays get a 16-byte zeroed plain allocation.
 int dalloc_index(int32_t** dst, const int32_t* src, size_t bytes) {
   *dst = nullptr;
