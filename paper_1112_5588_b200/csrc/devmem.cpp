@@ -119,7 +119,7 @@ bool vmm_alloc(void** out, size_t bytes, int device) {
 }  // namespace
 
 int set_compression(int mode) {
-  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "compression: 0 off, 1 generic compressible memory for col");
+  if (mode < 0 || mode > 1) return set_error(PJDS_ERR_INVALID_ARG, "compression: 0 off, 1 generic compressible memory for the int32 index arrays");
   g_compress = mode;
   return PJDS_OK;
 }
@@ -172,7 +172,7 @@ int dalloc_index(int32_t** dst, const int32_t* src, size_t bytes) {
     }
     cudaGetLastError();
     dev_free(p);
-    return set_error(PJDS_ERR_CUDA, std::string("compressible column-index upload: ") + cudaGetErrorString(e));
+    return set_error(PJDS_ERR_CUDA, std::string("compressible index-array upload: ") + cudaGetErrorString(e));
   }
   PJDS_CUDA_TRY(cudaMalloc((void**)dst, bytes ? bytes : 16));
   if (!bytes) PJDS_CUDA_TRY(cudaMemset(*dst, 0, 16));
