@@ -761,7 +761,7 @@ static bool g_il = false;    // lane-interleaved rows (variant knob unroll + 32;
 
 template <typename T, typename Off, int R, int U>
 int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode, double* dot_part, int64_t* nparts,
-                  bool pipe) {
+                  bool pipe, bool il_req = false) {
   const auto& h = A->h;
   const int64_t threads = h.n_pad / R;
   const int64_t grid = (threads + kThreads - 1) / kThreads;
@@ -780,11 +780,11 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   // 96 % of rows in one class, loses 16 % with it, and the permuted basis loses 1-3 %)
   const bool by_warp = (g_tile_order == 3 || (g_tile_order == 2 && A->mixed_classes &&
                                               (mode == STORE_PERM || mode == STORE_PERM_ACC))) &&
-                       h.n_windows <= 1 && !(g_il && R > 1) && !A->d_win;
+                       h.n_windows <= 1 && !(il_req && R > 1) && !A->d_win;
   const int* worder = by_warp ? A->d_worder[R == 4 ? 2 : (R == 2 ? 1 : 0)] : nullptr;
   const int64_t n_wtiles = (h.n_pad + 32 * R - 1) / (32 * R);
   // grids of a few waves: dynamic warp tiles (same row chains, bitwise the same y)
-  if (A->d_sched && h.n_windows <= 1 && !(g_il && R > 1) && mode != STORE_DIRECT_DOT && !by_warp) {
+  if (A->d_sched && h.n_windows <= 1 && !(il_req && R > 1) && mode != STORE_DIRECT_DOT && !by_warp) {
     bool done = false;
 int st;
     if (mode == STORE_DIRECT) st = launch_dyn_any<T, Off, R, U, STORE_DIRECT>(A, y, x, s, order, grid, pipe, &done);
@@ -820,7 +820,7 @@ int st;
       return set_error(PJDS_ERR_UNSUPPORTED, "window matrices need 32-bit jagged offsets");
     }
   }
-  const bool il = g_il && R > 1 && h.br % (32 * R) == 0;
+  const bool il = il_req && R > 1 && h.br % (32 * R) == 0;
 #define PJDS_LAUNCH(M)                    \
   if (pipe) PJDS_LAUNCH_PF(M, true, false); \
   else if (il) PJDS_LAUNCH_PF(M, false, true); \
@@ -881,6 +881,7 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
                                     : launch_pjds_split_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np);
     return launch_pjds_split_t<T, Off, 8, 4>(A, yy, xx, s, mode, dp, np);
   }
+  bool il = g_il;
   if (R == 0) {
     // enough warps to cover the SMs several times: R = 4 (256-bit DP loads) for large matrices,
     // R = 2 / 1 when n_pad / R would leave the GPU short of warps (long-row matrices like DLR1)
@@ -891,17 +892,24 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
     // long rows in SP (half the bytes per load): overlapping the next chunk's stream with the
     // current gathers pays (measured C4 SP +5 %, W4 SP +10 %; DP on C4 loses, so DP stays plain)
     pipe = sizeof(T) == 4 && R == 2;
+    // DP, permuted basis, R = 4 with 128-row blocks: lane-interleaved rows (one gather instruction
+    // covers 32 consecutive sorted rows).  With the index arrays compressed the kernel is no longer
+    // at the DRAM ceiling and the 4x fewer L1 gather wavefronts pay: C5 DP 1943-1952 -> 1922 us,
+    // C3 DP 190-192 -> 182.6, C2 DP 57.0 -> 53.6; SP loses on C3/C5 (115 -> 120, 1188 -> 1275)
+    // (profiles/r02_kbench_variants_compress.jsonl)
+    il = il || (sizeof(T) == 8 && R == 4 && mode == STORE_DIRECT && A->h.br % 128 == 0 && A->h.n_windows <= 1 &&
+                !A->d_win);
   }
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;
   const T* xx = (const T*)x;
   if (R == 4)
-    return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np, pipe)
-                  : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode, dp, np, pipe);
+    return U >= 4 ? launch_pjds_t<T, Off, 4, 4>(A, yy, xx, s, mode, dp, np, pipe, il)
+                  : launch_pjds_t<T, Off, 4, 2>(A, yy, xx, s, mode, dp, np, pipe, il);
   if (R == 2)
-    return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np, pipe)
-                  : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode, dp, np, pipe);
-  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode, dp, np, pipe);
+    return U >= 8 ? launch_pjds_t<T, Off, 2, 8>(A, yy, xx, s, mode, dp, np, pipe, il)
+                  : launch_pjds_t<T, Off, 2, 4>(A, yy, xx, s, mode, dp, np, pipe, il);
+  return launch_pjds_t<T, Off, 1, 8>(A, yy, xx, s, mode, dp, np, pipe, il);
 }
 
 template <typename T>

@@ -1,7 +1,10 @@
-# round 2, call 41: multi-GPU emulations with the final build (compressible index arrays, launch
-# overlap): the NCCL split under full contention, and DIRECT with R processes on one GPU
+# round 2, call 43: automatic lane-interleaved rows for DP permuted basis -- full GPU suite, then the
+# bench A/B (auto vs the plain R4U2 variant) alternating twice on one box
 set -x
-timeout 900 python tools/dist_emulate2.py --ranks 2,4,8 --modes rows --nl-sigma 1024 > gpurun_out/r02c41_dist_emul2.jsonl 2> gpurun_out/r02c41_dist_emul2.err
-for R in 1 2 4 8; do
-  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $R --master-addr 127.0.0.1 --master-port $((29870+R)) tools/direct_emulate.py C5 30 5 >> gpurun_out/r02c41_direct.jsonl 2>> gpurun_out/r02c41_direct.err
+python -m pytest tests -m gpu -x -q > gpurun_out/r02c43_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c43_gputests.txt
+for V in auto plain auto plain; do
+  if [ $V = auto ]; then A=""; else A="--variant 4,2"; fi
+  python bench.py --no-cpu-baseline $A > gpurun_out/r02c43_bench_$V.json.tmp 2>> gpurun_out/r02c43_bench.err
+  cat gpurun_out/r02c43_bench_$V.json.tmp >> gpurun_out/r02c43_bench_$V.jsonl
 done
+rm -f gpurun_out/*.tmp
