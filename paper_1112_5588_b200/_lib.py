@@ -7,7 +7,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpjds.so")
+LIB_PATH = os.environ.get("PJDS_LIB_PATH") or os.path.join(_HERE, "libpjds.so")  # override: dev A/B builds only
 
 PJDS_F32, PJDS_F64 = 0, 1
 PJDS_PERM_ROWS, PJDS_PERM_SYMMETRIC, PJDS_HOST_ONLY = 0, 1, 2

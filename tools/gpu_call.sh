@@ -1,10 +1,7 @@
-# round 2, call 43: automatic lane-interleaved rows for DP permuted basis -- full GPU suite, then the
-# bench A/B (auto vs the plain R4U2 variant) alternating twice on one box
+# round 2, call 44: lane-interleaved DP kernel at 5 resident CTAs/SM (48 registers, 8-byte spill)
+# vs the default (56 registers, 4 CTAs/SM), alternating
 set -x
-python -m pytest tests -m gpu -x -q > gpurun_out/r02c43_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c43_gputests.txt
-for V in auto plain auto plain; do
-  if [ $V = auto ]; then A=""; else A="--variant 4,2"; fi
-  python bench.py --no-cpu-baseline $A > gpurun_out/r02c43_bench_$V.json.tmp 2>> gpurun_out/r02c43_bench.err
-  cat gpurun_out/r02c43_bench_$V.json.tmp >> gpurun_out/r02c43_bench_$V.jsonl
+for L in default minb5 default minb5; do
+  if [ $L = minb5 ]; then export PJDS_LIB_PATH=$PWD/experiments/libpjds_ilminb5.so; else unset PJDS_LIB_PATH; fi
+  timeout 900 python tools/kbench.py --configs C5,C3,C2 --dtypes f64 --fmts pjds128s --reps 40 --rotate 2 | sed "s/^{/{\"lib\": \"$L\", /" >> gpurun_out/r02c44_minb.jsonl 2>> gpurun_out/r02c44_minb.err
 done
-rm -f gpurun_out/*.tmp
