@@ -356,11 +356,8 @@ __device__ __forceinline__ void row_chains(T (&acc)[R], const T* __restrict__ va
 // chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
 // WIN: fused remote-gather dist kernel (x = the owners' windows, see gather_x).
-#ifndef PJDS_IL_MINB
-#define PJDS_IL_MINB 1
-#endif
 template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false, bool WIN = false>
-__global__ void __launch_bounds__(kThreads, IL ? PJDS_IL_MINB : 1)
+__global__ void __launch_bounds__(kThreads)
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,
