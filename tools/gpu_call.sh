@@ -1,6 +1,4 @@
-# round 2, call 46: final-tree validation -- smoke, full GPU suite, default bench, reference arm
+# round 2, call 47: row-only basis (y stored through perm) with the lane-interleaved layout, now that
+# the index arrays are compressed; plain auto (warp-granular order) vs IL (CTA original-row order)
 set -x
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02c46_smoke.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c46_smoke.txt
-python -m pytest tests -m gpu -x -q > gpurun_out/r02c46_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c46_gputests.txt
-python bench.py > gpurun_out/r02c46_bench.json 2> gpurun_out/r02c46_bench.err
-python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r02c46_reference.json 2> gpurun_out/r02c46_reference.err
+timeout 1200 python tools/kbench.py --configs C5,C3,C2 --dtypes f64,f32 --fmts pjds128 --variants 0x0,4x34,0x0,4x34 --reps 40 --rotate 2 > gpurun_out/r02c47_rows_il.jsonl 2> gpurun_out/r02c47_rows_il.err
