@@ -808,9 +808,11 @@ int st;
       (const int*)A->d_perm, x, y, h.n, h.n_pad, (int)h.br, pol, order, dot_part, h.sigma,                  \
       (const int64_t*)A->d_wcs_off, (const T* const*)A->d_win, (int)A->win_shift, worder, n_wtiles))
 #define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
-  if (A->d_win) {  // fused remote-gather dist matrix: plain main loop, direct or perm store
+  const bool il = il_req && R > 1 && h.br % (32 * R) == 0;
+  if (A->d_win) {  // fused remote-gather dist matrix: plain (or lane-interleaved) main loop, direct or perm store
     if constexpr (std::is_same<Off, int32_t>::value) {
-      if (mode == STORE_DIRECT) PJDS_LAUNCH_W(STORE_DIRECT, false, false, true);
+      if (mode == STORE_DIRECT && il) PJDS_LAUNCH_W(STORE_DIRECT, false, true, true);
+      else if (mode == STORE_DIRECT) PJDS_LAUNCH_W(STORE_DIRECT, false, false, true);
       else if (mode == STORE_PERM) PJDS_LAUNCH_W(STORE_PERM, false, false, true);
       else return set_error(PJDS_ERR_UNSUPPORTED, "window matrices support y = A x only");
       count_launch();
@@ -820,7 +822,6 @@ int st;
       return set_error(PJDS_ERR_UNSUPPORTED, "window matrices need 32-bit jagged offsets");
     }
   }
-  const bool il = il_req && R > 1 && h.br % (32 * R) == 0;
 #define PJDS_LAUNCH(M)                    \
   if (pipe) PJDS_LAUNCH_PF(M, true, false); \
   else if (il) PJDS_LAUNCH_PF(M, false, true); \
@@ -897,8 +898,7 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
     // at the DRAM ceiling and the 4x fewer L1 gather wavefronts pay: C5 DP 1943-1952 -> 1922 us,
     // C3 DP 190-192 -> 182.6, C2 DP 57.0 -> 53.6; SP loses on C3/C5 (115 -> 120, 1188 -> 1275)
     // (profiles/r02_kbench_variants_compress.jsonl)
-    il = il || (sizeof(T) == 8 && R == 4 && mode == STORE_DIRECT && A->h.br % 128 == 0 && A->h.n_windows <= 1 &&
-                !A->d_win);
+    il = il || (sizeof(T) == 8 && R == 4 && mode == STORE_DIRECT && A->h.br % 128 == 0 && A->h.n_windows <= 1);
   }
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;

@@ -30,6 +30,7 @@ import paper_1112_5588_b200 as pj  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 calls = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+BR = int(sys.argv[4]) if len(sys.argv) > 4 else 32  # block rows of the DIRECT matrix and of T_1
 rank, R = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 torch.cuda.set_device(0)
 dist.init_process_group("gloo")
@@ -42,7 +43,7 @@ offs[-1] = n
 lo, hi = int(offs[rank]), int(offs[rank + 1])
 rp, col, val = g.crs(lo, hi)
 x_loc = inputs.vector(hi - lo, i0=lo)
-D = pj.DistPjds.create(n, offs, rp, col, val, permuted=True, transport="direct")
+D = pj.DistPjds.create(n, offs, rp, col, val, permuted=True, transport="direct", block_rows=BR)
 del col, val
 w = D.x_window()
 D.to_permuted(w, torch.from_numpy(x_loc).cuda())
@@ -88,7 +89,7 @@ x_full = inputs.vector(n) if R == 1 else None
 t_plain = None
 if R == 1:
     rp1, col1, val1 = g.crs()
-    P = pj.PjdsMatrix.from_crs(n, rp1, col1, val1, block_rows=32, symmetric=True)
+    P = pj.PjdsMatrix.from_crs(n, rp1, col1, val1, block_rows=BR, symmetric=True)
     del col1, val1
     xp = torch.empty(n, dtype=torch.float64, device="cuda")
     P.to_permuted(xp, torch.from_numpy(x_full).cuda())
@@ -102,7 +103,7 @@ recs = [None] * R
 dist.all_gather_object(recs, rec)
 if rank == 0:
     tk = [r_["t_kernel_us"] for r_ in recs]
-    print(json.dumps({"config": cfg, "R": R, "t_kernel_max_us": max(tk), "t_kernel_sum_us": round(sum(tk), 1),
+    print(json.dumps({"config": cfg, "R": R, "block_rows": BR, "t_kernel_max_us": max(tk), "t_kernel_sum_us": round(sum(tk), 1),
                       "t_job_one_gpu_us": recs[0]["t_job_us"],
                       "protocol_overhead_per_call_us": round(recs[0]["t_job_us"] - sum(tk), 1),
                       "all_finite": all(r_["finite"] for r_ in recs),

@@ -1,4 +1,7 @@
-# round 2, call 47: row-only basis (y stored through perm) with the lane-interleaved layout, now that
-# the index arrays are compressed; plain auto (warp-granular order) vs IL (CTA original-row order)
+# round 2, call 48: DIRECT transport with the lane-interleaved DP kernel at b_r 128 -- its tests
+# (bench N>1 legs, fake-NCCL / multi-process DIRECT) and the one-GPU emulation at b_r 128
 set -x
-timeout 1200 python tools/kbench.py --configs C5,C3,C2 --dtypes f64,f32 --fmts pjds128 --variants 0x0,4x34,0x0,4x34 --reps 40 --rotate 2 > gpurun_out/r02c47_rows_il.jsonl 2> gpurun_out/r02c47_rows_il.err
+python -m pytest tests/test_gpu_bench_dist.py tests/test_gpu_fake_nccl.py -x -q > gpurun_out/r02c48_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c48_tests.txt
+for R in 1 2 4 8; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $R --master-addr 127.0.0.1 --master-port $((29880+R)) tools/direct_emulate.py C5 30 5 128 >> gpurun_out/r02c48_direct_br128.jsonl 2>> gpurun_out/r02c48_direct.err
+done
