@@ -356,8 +356,15 @@ __device__ __forceinline__ void row_chains(T (&acc)[R], const T* __restrict__ va
 // chunk's x gathers) -- for long rows, whose chunks otherwise cost two dependent round trips each.
 // Per row: acc = +0; for j < block_len: acc = fma(val[col_start[j]+k], x[col[...]], acc).
 // WIN: fused remote-gather dist kernel (x = the owners' windows, see gather_x).
+// dev experiments only (-DPJDS_IL_MINB=n): minimum resident CTAs for the lane-interleaved kernels;
+// the default build gives every kernel plain __launch_bounds__(kThreads) (ptxas: 48 / 56 registers)
+#ifdef PJDS_IL_MINB
+#define PJDS_KERNEL_BOUNDS __launch_bounds__(kThreads, IL ? PJDS_IL_MINB : 4)
+#else
+#define PJDS_KERNEL_BOUNDS __launch_bounds__(kThreads)
+#endif
 template <typename T, typename Off, int R, int U, int MODE, bool PIPE, bool IL = false, bool WIN = false>
-__global__ void __launch_bounds__(kThreads)
+__global__ void PJDS_KERNEL_BOUNDS
 pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const int64_t* __restrict__ col_start,
                  const int* __restrict__ block_len, const int* __restrict__ perm, const T* __restrict__ x,
                  T* __restrict__ y, int64_t n, int64_t n_pad, int br, int pol, const int* __restrict__ tile_order,

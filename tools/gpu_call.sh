@@ -1,7 +1,8 @@
-# round 2, call 48: DIRECT transport with the lane-interleaved DP kernel at b_r 128 -- its tests
-# (bench N>1 legs, fake-NCCL / multi-process DIRECT) and the one-GPU emulation at b_r 128
+# round 2, call 49: occupancy of the lane-interleaved DP kernel -- default build (56 registers,
+# 4 CTAs/SM) vs dev builds with __launch_bounds__ min 5 (48 regs, 8 B spill) and 6 (40 regs, spills),
+# alternating (build/alt/*.so, PJDS_LIB_PATH)
 set -x
-python -m pytest tests/test_gpu_bench_dist.py tests/test_gpu_fake_nccl.py -x -q > gpurun_out/r02c48_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c48_tests.txt
-for R in 1 2 4 8; do
-  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $R --master-addr 127.0.0.1 --master-port $((29880+R)) tools/direct_emulate.py C5 30 5 128 >> gpurun_out/r02c48_direct_br128.jsonl 2>> gpurun_out/r02c48_direct.err
+for L in default minb5 minb6 default minb5 minb6; do
+  if [ $L = default ]; then unset PJDS_LIB_PATH; else export PJDS_LIB_PATH=$PWD/build/alt/libpjds_$L.so; fi
+  timeout 900 python tools/kbench.py --configs C5,C3,C2 --dtypes f64 --fmts pjds128s --reps 40 --rotate 2 | sed "s/^{/{\"lib\": \"$L\", /" >> gpurun_out/r02c49_minb.jsonl 2>> gpurun_out/r02c49_minb.err
 done
