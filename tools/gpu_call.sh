@@ -1,8 +1,4 @@
-# round 2, call 49: occupancy of the lane-interleaved DP kernel -- default build (56 registers,
-# 4 CTAs/SM) vs dev builds with __launch_bounds__ min 5 (48 regs, 8 B spill) and 6 (40 regs, spills),
-# alternating (build/alt/*.so, PJDS_LIB_PATH)
+# round 2, call 50: the one-wave DLR1 matrix (C4) with compression + launch overlap: variant sweep
+# incl. the long-row split-j kernel, x/y rotated
 set -x
-for L in default minb5 minb6 default minb5 minb6; do
-  if [ $L = default ]; then unset PJDS_LIB_PATH; else export PJDS_LIB_PATH=$PWD/build/alt/libpjds_$L.so; fi
-  timeout 900 python tools/kbench.py --configs C5,C3,C2 --dtypes f64 --fmts pjds128s --reps 40 --rotate 2 | sed "s/^{/{\"lib\": \"$L\", /" >> gpurun_out/r02c49_minb.jsonl 2>> gpurun_out/r02c49_minb.err
-done
+timeout 1200 python tools/kbench.py --configs C4 --dtypes f32,f64 --fmts pjds128s --variants 0x0,1x8,1x4,2x8,2x20,18x4,18x8,20x4,0x0 --reps 120 --rotate 64 > gpurun_out/r02c50_c4.jsonl 2> gpurun_out/r02c50_c4.err
