@@ -172,3 +172,25 @@ def test_gpu_lanczos_split_variant():
             assert np.abs(b[:10] - rb[:10]).max() <= 1e-10 * scale, S
     finally:
         L.pjds_set_kernel_variant(0, 0)
+
+
+@pytest.mark.gpu
+def test_gpu_lanczos_c3_br128_lane_interleaved():
+    """C3-sized symmetric HMEp matrix at b_r = 128 in DP: the Lanczos product runs the
+    lane-interleaved kernel with the fused alpha partials (R = 4, rows 32 apart per thread); its
+    coefficients follow the oracle recurrence (scipy CSR products) over 12 steps."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    import paper_1112_5588_b200 as pj
+    n, rp, col, val = inputs.config_crs("C3", symmetric=True)
+    v0 = inputs.vector(n, np.float64, seed=79)
+    A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=128, symmetric=True)
+    perm = A.export()["perm"]
+    m = 12
+    a, b, steps = A.lanczos(torch.from_numpy(v0[perm].copy()).cuda(), m)
+    assert steps == m
+    ra, rb = olz.lanczos(n, rp, col, val, v0, m)
+    scale = max(np.abs(ra).max(), np.abs(rb).max())
+    assert np.abs(a - ra).max() <= 1e-12 * scale
+    assert np.abs(b - rb).max() <= 1e-12 * scale

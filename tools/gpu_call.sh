@@ -1,4 +1,8 @@
-# round 2, call 50: the one-wave DLR1 matrix (C4) with compression + launch overlap: variant sweep
-# incl. the long-row split-j kernel, x/y rotated
+# round 2, call 51: the Lanczos fused-dot product with the lane-interleaved DP layout at b_r 128 --
+# Lanczos GPU tests, per-step device times at b_r 32 and 128
 set -x
-timeout 1200 python tools/kbench.py --configs C4 --dtypes f32,f64 --fmts pjds128s --variants 0x0,1x8,1x4,2x8,2x20,18x4,18x8,20x4,0x0 --reps 120 --rotate 64 > gpurun_out/r02c50_c4.jsonl 2> gpurun_out/r02c50_c4.err
+python -m pytest tests/test_lanczos.py -x -q > gpurun_out/r02c51_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c51_tests.txt
+for BR in 32 128; do
+  timeout 900 python tools/lanczos_bench.py C5 50 $BR >> gpurun_out/r02c51_lanczos.jsonl 2>> gpurun_out/r02c51_lanczos.err
+  timeout 600 python tools/lanczos_bench.py C3 200 $BR >> gpurun_out/r02c51_lanczos.jsonl 2>> gpurun_out/r02c51_lanczos.err
+done

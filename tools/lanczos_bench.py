@@ -9,8 +9,9 @@ import inputs
 import paper_1112_5588_b200 as pj
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 m = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+br = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 n, rp, col, val = inputs.config_crs(cfg, symmetric=True)
-A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True)
+A = pj.PjdsMatrix.from_crs(n, rp, col, val, symmetric=True, block_rows=br)
 nnz = len(col)
 del rp, col, val
 v0 = torch.from_numpy(inputs.vector(n, seed=77)).cuda()
@@ -43,6 +44,6 @@ for e in kern:
     busy[key] = busy.get(key, 0.0) + (e.time_range.end - e.time_range.start) * 1e-6
 print(json.dumps({"device_span_per_step_ms": round(span / m * 1e3, 4), "device_overhead_frac": round(span / ts - 1, 3),
                   "kernel_ms_per_step": {k: round(v / m * 1e3, 4) for k, v in busy.items()}, "n_kernels": len(kern)}))
-print(json.dumps({"config": cfg, "m": m, "steps": steps, "lanczos_s": round(t, 4), "per_step_ms": round(t / m * 1e3, 3),
+print(json.dumps({"config": cfg, "block_rows": br, "m": m, "steps": steps, "lanczos_s": round(t, 4), "per_step_ms": round(t / m * 1e3, 3),
                   "spmv_only_per_step_ms": round(ts / m * 1e3, 3), "overhead_frac": round(t / ts - 1, 3),
                   "spmv_gflops_in_lanczos": round(2 * nnz * m / t / 1e9, 1), "ritz_min": ev[0], "ritz_max": ev[-1]}))
