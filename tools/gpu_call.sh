@@ -1,8 +1,6 @@
-# round 2, call 51: the Lanczos fused-dot product with the lane-interleaved DP layout at b_r 128 --
-# Lanczos GPU tests, per-step device times at b_r 32 and 128
+# round 2, call 52: final-tree validation after the DIRECT / Lanczos lane-interleaved changes --
+# smoke, full GPU suite, default bench
 set -x
-python -m pytest tests/test_lanczos.py -x -q > gpurun_out/r02c51_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c51_tests.txt
-for BR in 32 128; do
-  timeout 900 python tools/lanczos_bench.py C5 50 $BR >> gpurun_out/r02c51_lanczos.jsonl 2>> gpurun_out/r02c51_lanczos.err
-  timeout 600 python tools/lanczos_bench.py C3 200 $BR >> gpurun_out/r02c51_lanczos.jsonl 2>> gpurun_out/r02c51_lanczos.err
-done
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02c52_smoke.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c52_smoke.txt
+python -m pytest tests -m gpu -x -q > gpurun_out/r02c52_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c52_gputests.txt
+python bench.py > gpurun_out/r02c52_bench.json 2> gpurun_out/r02c52_bench.err
