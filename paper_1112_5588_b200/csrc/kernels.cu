@@ -905,8 +905,10 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
     // at the DRAM ceiling and the 4x fewer L1 gather wavefronts pay: C5 DP 1943-1952 -> 1922 us,
     // C3 DP 190-192 -> 182.6, C2 DP 57.0 -> 53.6; SP loses on C3/C5 (115 -> 120, 1188 -> 1275)
     // (profiles/r02_kbench_variants_compress.jsonl)
-    il = il || (sizeof(T) == 8 && R == 4 && (mode == STORE_DIRECT || mode == STORE_DIRECT_DOT) &&
-                A->h.br % 128 == 0 && A->h.n_windows <= 1);
+    // SP: only when one length class holds >= 90 % of the rows (consecutive sorted rows are then
+    // nearly consecutive original rows; sAMG C2 SP 35.1 -> 33.0 us), not on the mixed-class HMEp
+    il = il || ((sizeof(T) == 8 || !A->mixed_classes) && R == 4 &&
+                (mode == STORE_DIRECT || mode == STORE_DIRECT_DOT) && A->h.br % 128 == 0 && A->h.n_windows <= 1);
   }
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;
