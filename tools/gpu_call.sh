@@ -1,6 +1,4 @@
-# round 2, call 54: final-tree validation after the SP lane-interleaving rule -- smoke, full GPU
-# suite, default bench
+# round 2, call 55: row-only basis tile orders under compression (0 storage, 1 CTA original-row,
+# 3 warp-granular = auto for mixed classes)
 set -x
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02c54_smoke.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c54_smoke.txt
-python -m pytest tests -m gpu -x -q > gpurun_out/r02c54_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c54_gputests.txt
-python bench.py > gpurun_out/r02c54_bench.json 2> gpurun_out/r02c54_bench.err
+timeout 1200 python tools/kbench.py --configs C5,C3 --dtypes f64,f32 --fmts pjds128 --orders 3,1,0,3,1 --reps 40 --rotate 2 > gpurun_out/r02c55_rows_orders.jsonl 2> gpurun_out/r02c55_rows_orders.err
