@@ -382,13 +382,13 @@ pjds_spmv_kernel(const T* __restrict__ val, const int* __restrict__ col, const i
   constexpr int RS = IL ? 32 : 1;  // distance between a thread's rows
   int64_t k0, cta_k0;
   int cta_len;
-  if (!IL && warp_order) {
+  if (warp_order) {
     // warp-granular order (tile order mode 3): each warp takes the warp tile (32 R consecutive
     // sorted rows) the table assigns to its slot, so one CTA runs warp tiles of several length
     // classes from one region of the original matrix; staged col_start covers the widest (block 0)
     const int64_t slot = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
     const int64_t wt = slot < n_wtiles ? (int64_t)warp_order[slot] : (n_pad / (32 * R) + 1);
-    k0 = wt * 32 * R + (int64_t)(threadIdx.x & 31) * R;
+    k0 = wt * 32 * R + (int64_t)(threadIdx.x & 31) * (IL ? 1 : R);
     cta_k0 = 0;
     cta_len = block_len[0];
   } else {
@@ -785,9 +785,10 @@ int launch_pjds_t(const pjds_mat* A, T* y, const T* x, cudaStream_t s, int mode,
   // warp-granular order (mode 3; auto: the row-only / accumulate stores when no length class
   // dominates -- measured C5 DP rows-only 2384 -> 2256 us, C3 253 -> 238, C4 84 -> 81; the sAMG C2,
   // 96 % of rows in one class, loses 16 % with it, and the permuted basis loses 1-3 %)
+  const bool il = il_req && R > 1 && h.br % (32 * R) == 0;
   const bool by_warp = (g_tile_order == 3 || (g_tile_order == 2 && A->mixed_classes &&
                                               (mode == STORE_PERM || mode == STORE_PERM_ACC))) &&
-                       h.n_windows <= 1 && !(il_req && R > 1) && !A->d_win;
+                       h.n_windows <= 1 && !A->d_win;
   const int* worder = by_warp ? A->d_worder[R == 4 ? 2 : (R == 2 ? 1 : 0)] : nullptr;
   const int64_t n_wtiles = (h.n_pad + 32 * R - 1) / (32 * R);
   // grids of a few waves: dynamic warp tiles (same row chains, bitwise the same y)
@@ -815,7 +816,6 @@ int st;
       (const int*)A->d_perm, x, y, h.n, h.n_pad, (int)h.br, pol, order, dot_part, h.sigma,                  \
       (const int64_t*)A->d_wcs_off, (const T* const*)A->d_win, (int)A->win_shift, worder, n_wtiles))
 #define PJDS_LAUNCH_PF(M, PF, IL) PJDS_LAUNCH_W(M, PF, IL, false)
-  const bool il = il_req && R > 1 && h.br % (32 * R) == 0;
   if (A->d_win) {  // fused remote-gather dist matrix: plain (or lane-interleaved) main loop, direct or perm store
     if constexpr (std::is_same<Off, int32_t>::value) {
       if (mode == STORE_DIRECT && il) PJDS_LAUNCH_W(STORE_DIRECT, false, true, true);
@@ -907,8 +907,10 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
     // (profiles/r02_kbench_variants_compress.jsonl)
     // SP: only when one length class holds >= 90 % of the rows (consecutive sorted rows are then
     // nearly consecutive original rows; sAMG C2 SP 35.1 -> 33.0 us), not on the mixed-class HMEp
-    il = il || ((sizeof(T) == 8 || !A->mixed_classes) && R == 4 &&
-                (mode == STORE_DIRECT || mode == STORE_DIRECT_DOT) && A->h.br % 128 == 0 && A->h.n_windows <= 1);
+    // The same rule for the row-only / y += stores, whose warp-granular order now takes interleaved
+    // rows inside each warp tile: C3 DP 223 -> 215 us, C2 DP 65.2 -> 63.7, C5 DP unchanged; SP
+    // C2 39.3 -> 37.6 but C5 SP 1356-1365 -> 1364-1414 (profiles/r02_kbench_rows_il_worder.jsonl)
+    il = il || ((sizeof(T) == 8 || !A->mixed_classes) && R == 4 && A->h.br % 128 == 0 && A->h.n_windows <= 1);
   }
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;

@@ -491,13 +491,21 @@ def test_warp_tile_order_variants_bitwise(pj, dtype):
                 for sym in (False, True):
                     A = pj.PjdsMatrix.from_crs(n, rp, col, val, block_rows=br, symmetric=sym)
                     xin = A.to_permuted(torch.empty_like(xt), xt) if sym else xt
-                    for variant in ((0, 0), (1, 8), (2, 4), (4, 2), (4, 4)):
+                    # (4, 34) / (2, 36): lane-interleaved rows inside the warp tiles (b_r 128 only)
+                    for variant in ((0, 0), (1, 8), (2, 4), (4, 2), (4, 4), (4, 34), (2, 36)):
                         assert L.pjds_set_kernel_variant(*variant) == 0
                         y = torch.full_like(xt, float("nan"))
                         A.spmv(y, xin)
                         yo = A.from_permuted(torch.empty_like(y), y) if sym else y
                         torch.cuda.synchronize()
                         check_y(yo.cpu().numpy(), n, rp, col, val, x)
+                        if not sym:  # y += A x through the warp tiles as well
+                            y0 = inputs.vector(n, dtype, seed=93)
+                            ya = tdev(y0)
+                            A.spmv_accum(ya, xin)
+                            torch.cuda.synchronize()
+                            want = (y0 + oracle.spmv_chain(n, rp, col, val, x)).astype(dtype)
+                            assert np.array_equal(ya.cpu().numpy(), want), (name, br, variant)
                     del A
     finally:
         L.pjds_set_kernel_variant(0, 0)
