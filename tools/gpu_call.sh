@@ -1,5 +1,6 @@
-# round 2, call 57: lane-interleaved rows inside the warp-granular order (row-only / y += stores):
-# bitwise tests, then the row-only sweep plain vs interleaved under the automatic order
+# round 2, call 58: final-tree validation after extending lane interleaving to the row-only / y +=
+# stores -- smoke, full GPU suite, default bench
 set -x
-python -m pytest tests -m gpu -x -q -k "warp_tile_order or tile_order_bitwise or y_store or kernel_variants" > gpurun_out/r02c57_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c57_tests.txt
-timeout 1200 python tools/kbench.py --configs C5,C3,C2 --dtypes f64,f32 --fmts pjds128 --variants 0x0,4x34,0x0,4x34 --reps 40 --rotate 2 > gpurun_out/r02c57_rows_il_worder.jsonl 2> gpurun_out/r02c57_rows.err
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02c58_smoke.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c58_smoke.txt
+python -m pytest tests -m gpu -x -q > gpurun_out/r02c58_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c58_gputests.txt
+python bench.py > gpurun_out/r02c58_bench.json 2> gpurun_out/r02c58_bench.err
