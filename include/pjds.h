@@ -430,9 +430,9 @@ int pjds_bw_probe(int64_t bytes, int32_t reps, double* copy_gbs, double* read_gb
    32 apart, so one gather instruction covers 32 consecutive sorted rows; needs block_rows % 32R
    == 0).  The automatic choice (0, 0): R = 4, U = 2 for n_pad / 4 >= 2^19, else R = 2, U = 4
    (software-pipelined in SP), else R = 1, U = 8; lane-interleaved at R = 4 with block_rows a
-   multiple of 128 for every DP product (both bases, y += A x, the Lanczos fused-dot product, the
-   DIRECT window kernel; inside the warp tiles of the warp-granular order) and for SP products when
-   one length class holds >= 90 % of the rows. */
+   multiple of 128 for DP products (the permuted basis, the Lanczos fused-dot product, the DIRECT
+   window kernel; the row-only basis and y += A x when x is at most 64 MB, inside the warp tiles of
+   the warp-granular order) and for SP products when one length class holds >= 90 % of the rows. */
 int pjds_set_kernel_variant(int32_t rows_per_thread, int32_t unroll);
 
 /* Execution order of the CTA tiles of one handle (used whenever the tile order is on: mode 1, or

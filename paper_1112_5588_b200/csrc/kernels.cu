@@ -908,9 +908,12 @@ int launch_pjds_off(const pjds_mat* A, void* y, const void* x, cudaStream_t s, i
     // SP: only when one length class holds >= 90 % of the rows (consecutive sorted rows are then
     // nearly consecutive original rows; sAMG C2 SP 35.1 -> 33.0 us), not on the mixed-class HMEp
     // The same rule for the row-only / y += stores, whose warp-granular order now takes interleaved
-    // rows inside each warp tile: C3 DP 223 -> 215 us, C2 DP 65.2 -> 63.7, C5 DP unchanged; SP
-    // C2 39.3 -> 37.6 but C5 SP 1356-1365 -> 1364-1414 (profiles/r02_kbench_rows_il_worder.jsonl)
-    il = il || ((sizeof(T) == 8 || !A->mixed_classes) && R == 4 && A->h.br % 128 == 0 && A->h.n_windows <= 1);
+    // rows inside each warp tile, while x fits the 64 MB the tile-order rule uses: C3 DP 223 -> 215
+    // us, C2 DP 65.2 -> 63.7, C2 SP 39.3 -> 37.6; on C5 (x 456 MB) neutral warm and 3.4 % slower cold
+    // (2003 -> 2071 us under ncu), so plain there (profiles/r02_kbench_rows_il_worder.jsonl)
+    const bool perm_store = mode == STORE_PERM || mode == STORE_PERM_ACC;
+    il = il || ((sizeof(T) == 8 || !A->mixed_classes) && R == 4 && A->h.br % 128 == 0 && A->h.n_windows <= 1 &&
+                (!perm_store || A->ncols * (int64_t)sizeof(T) <= (int64_t(64) << 20)));
   }
   while (A->h.br % R) R >>= 1;  // R must divide b_r
   T* yy = (T*)y;

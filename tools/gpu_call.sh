@@ -1,6 +1,3 @@
-# round 2, call 58: final-tree validation after extending lane interleaving to the row-only / y +=
-# stores -- smoke, full GPU suite, default bench
+# round 2, call 59: ncu DRAM traffic of every kernel the bench line reports, final build
 set -x
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02c58_smoke.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c58_smoke.txt
-python -m pytest tests -m gpu -x -q > gpurun_out/r02c58_gputests.txt 2>&1; echo "rc=$?" >> gpurun_out/r02c58_gputests.txt
-python bench.py > gpurun_out/r02c58_bench.json 2> gpurun_out/r02c58_bench.err
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:spmv --csv --log-file gpurun_out/r02c59_traffic.csv python tools/traffic_capture.py > gpurun_out/r02c59_traffic_order.txt 2>&1
